@@ -1,0 +1,163 @@
+/*
+ * oracle.c -- plain, slow, double-precision CPU oracle for the segmentation hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_1912_11494_b200/) never links, imports or executes it, and this file
+ * shares no code, header, table or constant generator with the CUDA path.
+ *
+ * What it computes is the plain definition of the method's result (SURVEY.md
+ * Sec. 8(c), steps 1-6); the method's discard cascade (test1..test4,
+ * PAPER.md:97-99) is sound pruning and therefore reaches this same result, so the
+ * oracle evaluates every (fiber, centroid) pair with no discarding, no blocking
+ * and no reordering:
+ *
+ *   Eq. 1 (Sec. 2.3):  d_E(a_i, b_i) = || a_i - b_i ||_2
+ *   Eq. 2 (Sec. 2.3):  d_ME(a, b) = min( max_i d_E(a_i, b_i),
+ *                                                      max_i d_E(a_i, b_{N-i}) )
+ *          with 0-based indices, b_{N-i} read as b_{20-i} (reading R1),
+ *   labelling (Alg. 1 lines 13-16; "only the
+ *          closest bundle"; PAPER.md:64 per-bundle threshold):
+ *          label(a) = argmin_b { D_b(a) : D_b(a) <= thr_b },  D_b = min_{c in b} d_ME(a, c),
+ *          ties -> lowest bundle id (Alg. 1 updates on strict '<' with j ascending,
+ *          PAPER.md:130, reading R5), -1 when no bundle qualifies (reading R8).
+ *
+ * Arithmetic: every FP32 input is promoted to double; squared distances are
+ * compared (monotone, so the argmin/threshold decisions equal those on distances);
+ * dist = sqrt(D^2) of the winner, +inf when unlabelled, NaN for a non-finite fiber
+ * (reading R12).
+ *
+ * Tie band (BASELINE.json north_star "1e-3 mm from its
+ * threshold and from the runner-up bundle"): decidable[n] = 1 iff the fiber's label
+ * is not within delta of a threshold or of a runner-up bundle; only decidable
+ * fibers are held to exact label equality by the parity tests.
+ *
+ * Parity pins: tests/test_oracle_pins.py (closed forms, SPEC worked examples under
+ * tests/golden/, invariants, a library special case, brute force on tiny inputs).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#define NPTS 21
+
+/* Eq. 1, squared: ||p - q||^2 in double. */
+double oracle_point_d2(const float *p, const float *q)
+{
+    double dx = (double)p[0] - (double)q[0];
+    double dy = (double)p[1] - (double)q[1];
+    double dz = (double)p[2] - (double)q[2];
+    return dx * dx + dy * dy + dz * dz;
+}
+
+/* One inner term of Eq. 2, squared: max_i d_E(a_i, b_i)^2 (inverse = 0) or
+ * max_i d_E(a_i, b_{20-i})^2 (inverse = 1). */
+double oracle_max_pointwise_d2(const float *a, const float *b, int inverse)
+{
+    double m = 0.0;
+    for (int i = 0; i < NPTS; i++) {
+        int j = inverse ? (NPTS - 1 - i) : i;
+        double d2 = oracle_point_d2(a + 3 * i, b + 3 * j);
+        if (d2 > m)
+            m = d2;
+    }
+    return m;
+}
+
+/* Eq. 2, squared: min over the direct and the inverse orientation. */
+double oracle_dme_d2(const float *a, const float *b)
+{
+    double dd = oracle_max_pointwise_d2(a, b, 0);
+    double di = oracle_max_pointwise_d2(a, b, 1);
+    return dd < di ? dd : di;
+}
+
+/* Eq. 2 in mm. */
+double oracle_dme(const float *a, const float *b)
+{
+    return sqrt(oracle_dme_d2(a, b));
+}
+
+static int fiber_is_finite(const float *f)
+{
+    for (int i = 0; i < 3 * NPTS; i++)
+        if (!isfinite(f[i]))
+            return 0;
+    return 1;
+}
+
+/*
+ * Classify n fibers against the atlas by the plain definition.
+ *   fibers     float [n][21][3]
+ *   centroids  float [M][21][3], bundle_id int32 [M] in [0, B), thresh float [B]
+ *   delta      tie-band half width in mm (1e-3 for the parity tests)
+ * Outputs (caller-owned, length n): label int32, dist double, decidable uint8;
+ *   d2b (nullable) double [n][B] = per-bundle minimum of d_ME^2 (+inf for an empty bundle).
+ * Returns 0, or -1 on invalid arguments (a bundle id out of range).
+ */
+int oracle_classify(const float *fibers, int64_t n,
+                    const float *centroids, const int32_t *bundle_id, int64_t M,
+                    const float *thresh, int32_t B, double delta,
+                    int32_t *label, double *dist, uint8_t *decidable, double *d2b)
+{
+    for (int64_t m = 0; m < M; m++)
+        if (bundle_id[m] < 0 || bundle_id[m] >= B)
+            return -1;
+    double *Db = (double *)malloc(sizeof(double) * (size_t)B);
+    if (!Db)
+        return -1;
+    for (int64_t f = 0; f < n; f++) {
+        const float *a = fibers + (size_t)f * 3 * NPTS;
+        /* step 2-3: per-bundle minimum of d_ME^2 over all centroids, no discarding */
+        for (int32_t b = 0; b < B; b++)
+            Db[b] = INFINITY;
+        for (int64_t m = 0; m < M; m++) {
+            double d2 = oracle_dme_d2(a, centroids + (size_t)m * 3 * NPTS);
+            if (d2 < Db[bundle_id[m]])
+                Db[bundle_id[m]] = d2;
+        }
+        if (d2b)
+            for (int32_t b = 0; b < B; b++)
+                d2b[(size_t)f * B + b] = Db[b];
+        if (!fiber_is_finite(a)) {
+            label[f] = -1;
+            dist[f] = NAN;
+            decidable[f] = 1;
+            continue;
+        }
+        /* step 4-5: accepted set {b : D_b^2 <= thr_b^2}; closest, ties -> lowest b */
+        int32_t best = -1;
+        for (int32_t b = 0; b < B; b++) {
+            double t = (double)thresh[b];
+            if (Db[b] <= t * t && (best < 0 || Db[b] < Db[best]))
+                best = b;
+        }
+        label[f] = best;
+        dist[f] = best < 0 ? INFINITY : sqrt(Db[best]);
+        /* step 6: tie band.  P = {b : d_b <= thr_b + delta}; b* = argmin_P d_b;
+         * decidable iff P empty, or d_b* < thr_b* - delta and every other b in P
+         * has d_b > d_b* + delta. */
+        int32_t bs = -1;
+        for (int32_t b = 0; b < B; b++) {
+            double d = sqrt(Db[b]);
+            if (d <= (double)thresh[b] + delta && (bs < 0 || d < sqrt(Db[bs])))
+                bs = b;
+        }
+        int ok = 1;
+        if (bs >= 0) {
+            double ds = sqrt(Db[bs]);
+            if (!(ds < (double)thresh[bs] - delta))
+                ok = 0;
+            for (int32_t b = 0; b < B && ok; b++) {
+                if (b == bs)
+                    continue;
+                double d = sqrt(Db[b]);
+                if (d <= (double)thresh[b] + delta && !(d > ds + delta))
+                    ok = 0;
+            }
+        }
+        decidable[f] = (uint8_t)ok;
+    }
+    free(Db);
+    return 0;
+}
