@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the segmentation hot path on B200 (BASELINE.json metric and config).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl reference]
+
+One step = one seg_classify of the whole workload (all rows a1-a9 of SURVEY.md Sec. 8(a)):
+config 3 by default, 4,145,000 synthetic fibers x the 62-bundle / 44,345-centroid atlas
+(BASELINE.json configs[3]; synthetic stand-ins).  Inputs are
+resident in HBM when the timed region starts; they are 1.04 GB (> 126 MB L2), so no L2
+flush is needed between steps.  Under torchrun each rank processes its own full-size
+subject (weak scaling, no data-path collective); the atlas is broadcast over NCCL at
+setup.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain C, double) on the box's host cores
+on a bounded seeded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fiber–centroid comparisons/sec"
+UNIT = "comparisons/s"
+FP32_LANES_PER_SM = 128          # B200 SM: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / guide)
+FP32_INSTR_PER_PDIST = 6         # Eq. 1 squared: 3 FADD + 1 FMUL + 2 FFMA
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stats", action="store_true", default=True)
+    return ap.parse_args()
+
+
+def workload_name(cfg):
+    from synth import CONFIGS
+    c = CONFIGS[cfg]
+    return (f"cfg{cfg}: {c['n_fibers']:,} fibers x {c['n_centroids']:,} centroids "
+            f"({c['n_bundles']} bundles), 21 pts, synthetic")
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------
+def time_oracle(cfg, fib, at, target_s):
+    import oracle
+    from synth import sample_indices
+    threads = os.cpu_count() or 1
+    # calibrate on a small sample, then size the timed sample for ~target_s
+    cal = fib[sample_indices(fib.shape[0], max(threads, 8), seed=77)]
+    t0 = time.perf_counter()
+    oracle.classify(cal, at.centroids, at.bundle_id, at.thresh, threads=threads)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    per_fiber = dt / cal.shape[0]
+    k = int(max(threads, min(fib.shape[0], target_s / per_fiber)))
+    idx = sample_indices(fib.shape[0], k, seed=78)
+    sub = fib[idx]
+    t0 = time.perf_counter()
+    oracle.classify(sub, at.centroids, at.bundle_id, at.thresh, threads=threads)
+    dt = time.perf_counter() - t0
+    n = sub.shape[0]
+    return dict(value=n * at.M / dt, unit=UNIT, cores=threads, kind="oracle",
+                fibers_per_s=n / dt, seconds=dt,
+                sample=f"{n} seeded fibers (synth.sample_indices seed 78) of {workload_name(cfg)} "
+                       f"against the full atlas; plain-definition oracle (fp64, no discarding), "
+                       f"{threads} host threads over contiguous fiber chunks")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth import atlas_for_config, fibers_for_config
+    at = atlas_for_config(args.config)
+    fib = fibers_for_config(args.config)
+    vals = []
+    budget = max(2.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        r = time_oracle(args.config, fib, at, budget)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * statistics.median([r["seconds"] for r in vals]),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=workload_name(args.config), sample=vals[-1]["sample"]),
+                fibers_per_s=statistics.median([r["fibers_per_s"] for r in vals]),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=vals[-1]["cores"], kind="oracle",
+                                  sample=vals[-1]["sample"]),
+                e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                gpu_launches=0)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (NVML, 10 ms period)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return dict(sm_mhz=None, sm_max_mhz=self.max_mhz, reasons=sorted(self.reasons), samples=0)
+        return dict(sm_mhz=float(statistics.median(self.samples)), sm_max_mhz=self.max_mhz,
+                    reasons=sorted(self.reasons), samples=len(self.samples))
+
+
+# ------------------------------------------------------------------------------------------
+# B200 arm
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1912_11494_b200 import Atlas, binding
+    from paper_1912_11494_b200.dist import broadcast_atlas
+    from synth import CONFIGS, atlas_for_config, fibers_for_config
+
+    cfg = args.config
+    spec = CONFIGS[cfg]
+    # atlas: rank 0 generates, NCCL broadcast to the others (setup, untimed)
+    at = atlas_for_config(cfg) if rank == 0 else None
+    cents, bid, thr = broadcast_atlas(at, spec["n_centroids"], spec["n_bundles"], dev, world)
+    atlas = Atlas(cents, bid, thr)
+    # this rank's subject (weak scaling: rank r segments subject r of the same shape)
+    workers = max(1, (os.cpu_count() or 1) // world)
+    t0 = time.perf_counter()
+    fib_np = fibers_for_config(cfg, subject=rank, workers=workers)
+    gen_s = time.perf_counter() - t0
+    N = fib_np.shape[0]
+    fib = torch.from_numpy(fib_np).to(dev)
+    lab = torch.empty(N, dtype=torch.int32, device=dev)
+    dst = torch.empty(N, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        atlas.classify(fib, lab, dst)
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: K steps ----------------
+    binding.seg_profile_enable(atlas.handle, args.steps)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            atlas.classify(fib, lab, dst)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    pre = np.zeros(args.steps, np.float32)
+    cls = np.zeros(args.steps, np.float32)
+    binding.seg_profile_read(atlas.handle, pre, cls, args.steps)
+    binding.seg_profile_enable(atlas.handle, 0)
+    t = torch.tensor([ms_total, float(cls.mean()), float(pre.mean())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, cls_ms, pre_ms = t.tolist()
+    ms_step = ms_total / args.steps
+    pairs = float(N) * spec["n_centroids"] * world
+    value = pairs / (ms_step * 1e-3)
+    fibers_per_s = N * world / (ms_step * 1e-3)
+    clocks = clk.summary()
+    launches_per_step = 4 if N >= 4096 else 1           # hist, scan, scatter, classify
+    res_lab = lab.cpu().numpy()
+
+    # ---------------- stage counters + roofline of the dominant kernel ----------------
+    _, _, st = atlas.classify_stats(fib)
+    torch.cuda.synchronize(dev)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz = clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965.0
+    w_instr = FP32_INSTR_PER_PDIST * st["lane_point_dists"]          # algorithmic FP32 lane-instr
+    achieved = w_instr / (cls_ms * 1e-3) / 1e12                      # T lane-instr / s
+    peak = sm_count * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"cfg{cfg}")
+        except Exception:
+            traffic = None
+    roofline = dict(bound="alu", achieved=achieved, peak=peak, unit="Tinstr/s (FP32 lane-instr)",
+                    frac=achieved / peak, traffic=traffic,
+                    kernel="k_classify", kernel_ms=cls_ms, prepass_ms=pre_ms,
+                    peak_basis=f"{sm_count} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_mhz:.0f} MHz "
+                               f"(median SM clock during the timed region)",
+                    work_basis=f"{FP32_INSTR_PER_PDIST} FP32 instr x {st['lane_point_dists']:,} lane point-distance "
+                               f"evaluations the kernel's rules needed (stats kernel, rank 0 subject)")
+
+    # ---------------- end to end: host buffers through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.from_numpy(fib_np).pin_memory()
+        hl = torch.empty(N, dtype=torch.int32).pin_memory()
+        hd = torch.empty(N, dtype=torch.float32).pin_memory()
+        atlas.classify(hf, hl, hd)                      # warm the host path
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            atlas.classify(hf, hl, hd)                  # H2D + classify + D2H, returns on completion
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+        assert np.array_equal(hl.numpy(), res_lab), "host-buffer path disagrees with device path"
+        e2e = dict(value=pairs / (e2e_ms * 1e-3), unit=UNIT, ms_per_step=e2e_ms,
+                   fibers_per_s=N * world / (e2e_ms * 1e-3),
+                   h2d_bytes_per_step=int(fib_np.nbytes), d2h_bytes_per_step=int(hl.numel() * 4 + hd.numel() * 4),
+                   steps=args.e2e_steps)
+
+    # ---------------- CPU baseline (oracle) on rank 0 at N=1 ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = time_oracle(cfg, fib_np, at, args.cpu_seconds)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f32",
+            data="synthetic",
+            config=dict(workload=workload_name(cfg), fibers_per_gpu=N, centroids=spec["n_centroids"],
+                        bundles=spec["n_bundles"], parallelism=f"fiber-sharded x{world} (one subject per rank)",
+                        l2="inputs 1.04 GB > 126 MB L2; no flush needed" if N * 252 > 126e6 else "inputs < L2",
+                        generator_s=round(gen_s, 1)),
+            fibers_per_s=fibers_per_s,
+            clocks=clocks, e2e=e2e, gpu_launches=launches_per_step * args.steps,
+            roofline=roofline, cpu_baseline=cpu,
+            cascade=st, labelled_frac=float((res_lab >= 0).mean()),
+        )
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

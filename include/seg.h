@@ -1,0 +1,165 @@
+/*
+ * seg.h -- C ABI of libsegb200.so, the B200 (sm_100a) hot path of atlas-based
+ * white-matter fiber segmentation (arXiv 1912.11494, "parallel segmentation",
+ * Alg. 1).
+ *
+ * What the library computes (reading list: DESIGN.md Sec. 3):
+ *   For every subject fiber a (21 points) and every atlas centroid c
+ *   (21 points) the maximum Euclidean distance of Eq. 2
+ *   (PAPER.md:73-76), min over the direct and the inverse point order:
+ *       d_ME(a, c) = min( max_i ||a_i - c_i||, max_i ||a_i - c_{20-i}|| ),  i = 0..20.
+ *   Each fiber is labelled with the bundle b of its closest centroid among the
+ *   centroids with d_ME <= thr_b (the per-bundle threshold; "only the
+ *   closest bundle"; Alg. 1 lines 13-16), ties to the
+ *   lowest bundle id, label -1 when no bundle qualifies.  The paper's progressive
+ *   discarding (test1 center point, test2 end points, test3 four points, test4 all 21
+ *   points with early exit) and an exact bundle/tile
+ *   lower-bound cull run inside the kernel; they are sound, so the result equals the
+ *   plain definition above (up to FP32 rounding of the distances).
+ *
+ * Arithmetic: FP32 on the CUDA cores (squared distances, no sqrt except for the
+ * returned distance, which is __fsqrt_rn of the winning squared distance).
+ *
+ * Data layout (all arrays C-contiguous, little endian):
+ *   fibers / centroids  float32 [n][21][3]   (x,y,z of point 0, point 1, ..., point 20), mm
+ *   bundle_id           int32   [M]          values in [0, B)
+ *   thresh              float32 [B]          mm, finite and > 0
+ *   label               int32   [N]          bundle id or -1
+ *   dist                float32 [N]          d_ME of the winner in mm; +inf when label = -1;
+ *                                            NaN (and label -1) for a fiber with a
+ *                                            non-finite coordinate
+ *
+ * Error behaviour: every entry point returns SEG_OK (0) or a negative code and then
+ * seg_last_error() (thread-local) describes the failure.  There is no CPU fallback:
+ * without a usable CUDA device the calls fail with SEG_ECUDA.
+ */
+#ifndef SEG_H
+#define SEG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEG_NPTS 21 /* points per fiber and per centroid */
+
+enum {
+    SEG_OK = 0,
+    SEG_EINVAL = -1, /* invalid argument (null pointer, size, range, alignment, non-finite) */
+    SEG_ENOMEM = -2, /* host or device allocation failed */
+    SEG_ECUDA = -3   /* CUDA runtime error or no usable device */
+};
+
+/* Opaque immutable atlas context living on one device. */
+typedef struct seg_atlas seg_atlas;
+
+/*
+ * seg_create -- build an atlas context on `device` (-1 = the calling thread's current
+ * device).  Groups centroids by bundle (the paper's atlasData[j]),
+ * orders each bundle spatially, cuts it into tiles of 32 centroids that never cross a
+ * bundle, and uploads the tiles plus per-tile / per-bundle bounding spheres of
+ * points 0, 10 and 20 (the exact lower bounds of the cull).
+ *   centroids  float32 [M][21][3], host or device memory (detected)
+ *   bundle_id  int32 [M] in [0, B), host or device memory
+ *   M >= 1, B >= 1; thresh float32 [B], finite and > 0 (host or device memory)
+ *   out        receives the context; set to NULL on error
+ * The library copies everything; the caller may free its inputs on return.
+ * Synchronous.  Bundles with no centroid are allowed (they never win).
+ * Errors: SEG_EINVAL (null pointer, M < 1, B < 1, bundle id out of range, threshold
+ * not finite or <= 0, non-finite centroid coordinate), SEG_ENOMEM, SEG_ECUDA.
+ */
+int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M,
+               const float *thresh, int32_t B, int device, seg_atlas **out);
+
+/*
+ * seg_classify -- label N fibers (Alg. 1 over all fibers).
+ *   fibers float32 [N][21][3]; label int32 [N]; dist float32 [N].
+ *   Either all three pointers are device memory on the atlas's device (the call is
+ *   then ASYNCHRONOUS on `stream`, a cudaStream_t; NULL = legacy default stream), or
+ *   all three are host memory (pinned or pageable): the call then streams chunks
+ *   host->device, classifies and copies the results back, overlapping the copies
+ *   with the kernel, and returns after the results are in host memory.
+ *   Internally a spatial-order prepass (Morton code of point 10) groups nearby fibers
+ *   into the same warps; results are scattered back to the caller's order.
+ *   Output is bitwise deterministic: independent of N, of the chunking, of the
+ *   stream, of the GPU count and of the order of centroids in seg_create.
+ *   Scratch is stream-ordered (cudaMallocAsync).  fibers needs 4-byte alignment.
+ *   N = 0 is a no-op returning SEG_OK.
+ * Errors: SEG_EINVAL (null atlas, null pointer with N > 0, N > 2^31 - 1, mixed host
+ * and device pointers, a device pointer on another device, misalignment),
+ * SEG_ENOMEM, SEG_ECUDA (launch failure).  Asynchronous execution faults surface
+ * at the caller's next synchronisation.
+ */
+int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
+                 int32_t *label, float *dist, void *stream);
+
+/* Number of counters written by seg_classify_stats. */
+#define SEG_NSTATS 12
+/*
+ * seg_classify_stats -- seg_classify (device pointers only) with the kernel's
+ * per-stage counters (SPEC.md:233-236 CascadeStats, extended), accumulated into the
+ * HOST array stats[SEG_NSTATS] after a stream synchronisation:
+ *   [0] fibers                [1] (warp, tile) pairs listed by the CTA pre-pass
+ *   [2] (warp, tile) pairs computed (some lane passed the tile bound)
+ *   [3] (lane, tile) pairs passing the tile bound    [4] lane midpoint tests (test1)
+ *   [5] lane endpoint tests (test2)                  [6] lane orientation passes into test3/4
+ *   [7] lane full 21-point completions               [8] best-distance updates (Alg. 1 l.15-16)
+ *   [9] lane point-distance evaluations (Eq. 1, all stages and the sphere bounds)
+ *   [10] lane sphere-bound tests (bundle + tile)     [11] CTAs
+ * A separate kernel instantiation; it computes the same labels and distances.
+ */
+int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,
+                       int32_t *label, float *dist, uint64_t *stats, void *stream);
+
+/* Shape of a built atlas (for tests and the bench). */
+typedef struct {
+    int64_t n_centroids;  /* M */
+    int32_t n_bundles;    /* B */
+    int32_t n_tiles;      /* tiles of 32 centroids (bundle-aligned, padded) */
+    int32_t tile_size;    /* 32 */
+    int32_t device;       /* CUDA ordinal */
+    int64_t device_bytes; /* device memory held by the context */
+} seg_atlas_info;
+
+int seg_get_atlas_info(const seg_atlas *atlas, seg_atlas_info *info);
+
+/*
+ * seg_plan_tiles -- the host half of seg_create, with no CUDA call: from HOST arrays
+ * computes the tile plan.  For tile t (t < *n_tiles, at most max_tiles written):
+ *   tile_bundle[t]          bundle id of the tile
+ *   tile_members[t*32 + k]  index into the caller's centroids of slot k (padding slots
+ *                           repeat a real member of the same bundle)
+ *   tile_spheres[t*12 + 4*s + {0,1,2,3}]  centre xyz and radius of the bounding sphere of
+ *                           point p_s over the tile's members, p = (0, 10, 20)
+ * Lets host tests check the cull's soundness invariant without a GPU.
+ * Errors: SEG_EINVAL as seg_create (host pointers only); SEG_ENOMEM.
+ */
+int seg_plan_tiles(const float *centroids, const int32_t *bundle_id, int64_t M, int32_t B,
+                   int32_t max_tiles, int32_t *n_tiles, int32_t *tile_bundle,
+                   int32_t *tile_members, float *tile_spheres);
+
+/*
+ * Profiling hook (bench.py only; NOT thread-safe, unlike the rest of the context):
+ * after seg_profile_enable(atlas, cap) the first `cap` device-pointer seg_classify calls
+ * on `atlas` record CUDA events on their stream before the spatial prepass, before the
+ * classify kernel and after it.  seg_profile_read synchronises on those events and writes,
+ * per recorded call i < min(count, capacity), prepass_ms[i] and classify_ms[i] (host arrays);
+ * *count receives the number of recorded calls.  cap = 0 disables and frees the events.
+ * Errors: SEG_EINVAL (null atlas, cap < 0), SEG_ECUDA.
+ */
+int seg_profile_enable(seg_atlas *atlas, int32_t capacity);
+int seg_profile_read(seg_atlas *atlas, float *prepass_ms, float *classify_ms, int32_t capacity,
+                     int32_t *count);
+
+/* Destroy a context (NULL-safe).  Must not race an in-flight seg_classify. */
+void seg_destroy(seg_atlas *atlas);
+
+/* Thread-local description of the last error ("" if none). */
+const char *seg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEG_H */

@@ -1,0 +1,118 @@
+"""B200-native hot path of atlas-based white-matter fiber segmentation (arXiv 1912.11494).
+
+    from paper_1912_11494_b200 import Atlas
+    atlas = Atlas(centroids, bundle_id, thresh)      # float32 [M,21,3], int32 [M], float32 [B]
+    label, dist = atlas.classify(fibers)             # float32 [N,21,3] torch CUDA tensor
+
+`binding` is the 1:1 ctypes binding of include/seg.h; `Atlas` only checks dtypes and
+shapes and passes raw pointers.  `dist` holds the multi-GPU driver.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import binding
+from .binding import SegError, STAT_NAMES  # noqa: F401
+
+__all__ = ["Atlas", "SegError", "binding"]
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _check_array(x, dtype_np, shape_tail, name):
+    if _is_torch(x):
+        import torch
+        want = {np.float32: torch.float32, np.int32: torch.int32}[dtype_np]
+        if x.dtype != want:
+            raise TypeError(f"{name}: dtype {x.dtype}, expected {want}")
+        if not x.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+    else:
+        if not isinstance(x, np.ndarray):
+            raise TypeError(f"{name}: expected a torch tensor or numpy array")
+        if x.dtype != dtype_np:
+            raise TypeError(f"{name}: dtype {x.dtype}, expected {np.dtype(dtype_np)}")
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: must be C-contiguous")
+    if tuple(x.shape[1:]) != tuple(shape_tail):
+        raise ValueError(f"{name}: shape {tuple(x.shape)}, expected [*, {', '.join(map(str, shape_tail))}]")
+
+
+class Atlas:
+    """An immutable atlas on one CUDA device (seg_create / seg_destroy)."""
+
+    def __init__(self, centroids, bundle_id, thresh, device: int = -1):
+        _check_array(centroids, np.float32, (21, 3), "centroids")
+        _check_array(bundle_id, np.int32, (), "bundle_id")
+        _check_array(thresh, np.float32, (), "thresh")
+        if bundle_id.shape[0] != centroids.shape[0]:
+            raise ValueError("bundle_id and centroids disagree on M")
+        self.M = int(centroids.shape[0])
+        self.B = int(thresh.shape[0])
+        self._h = binding.seg_create(centroids, bundle_id, self.M, thresh, self.B, device)
+        self.info = binding.seg_get_atlas_info(self._h)
+        self.device = self.info["device"]
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            binding.seg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _outputs(self, fibers, label, dist):
+        n = int(fibers.shape[0])
+        if _is_torch(fibers):
+            import torch
+            if label is None:
+                label = torch.empty(n, dtype=torch.int32, device=fibers.device)
+            if dist is None:
+                dist = torch.empty(n, dtype=torch.float32, device=fibers.device)
+        else:
+            if label is None:
+                label = np.empty(n, np.int32)
+            if dist is None:
+                dist = np.empty(n, np.float32)
+        _check_array(label, np.int32, (), "label")
+        _check_array(dist, np.float32, (), "dist")
+        if label.shape[0] != n or dist.shape[0] != n:
+            raise ValueError("label/dist length must equal the number of fibers")
+        return n, label, dist
+
+    @staticmethod
+    def _stream(fibers, stream):
+        if stream is not None:
+            return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+        if _is_torch(fibers) and fibers.is_cuda:
+            import torch
+            return int(torch.cuda.current_stream(fibers.device).cuda_stream)
+        return None
+
+    def classify(self, fibers, label=None, dist=None, stream=None):
+        """Label fibers [N,21,3] float32 -> (label int32[N], dist float32[N]).
+
+        CUDA tensors: asynchronous on `stream` (default: torch's current stream).
+        Host arrays/tensors: streamed through the device; returns when results are on the host.
+        """
+        _check_array(fibers, np.float32, (21, 3), "fibers")
+        n, label, dist = self._outputs(fibers, label, dist)
+        binding.seg_classify(self._h, fibers, n, label, dist, self._stream(fibers, stream))
+        return label, dist
+
+    def classify_stats(self, fibers, label=None, dist=None, stream=None):
+        """classify() through the counting kernel; returns (label, dist, {counter: value})."""
+        _check_array(fibers, np.float32, (21, 3), "fibers")
+        n, label, dist = self._outputs(fibers, label, dist)
+        stats = np.zeros(binding.SEG_NSTATS, np.uint64)
+        binding.seg_classify_stats(self._h, fibers, n, label, dist, stats, self._stream(fibers, stream))
+        return label, dist, dict(zip(binding.STAT_NAMES, (int(v) for v in stats)))

@@ -1,0 +1,131 @@
+"""Thin ctypes binding of libsegb200.so (include/seg.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  There is no CPU fallback -- if the library cannot be loaded the import
+of this module fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _build
+
+SEG_OK, SEG_EINVAL, SEG_ENOMEM, SEG_ECUDA = 0, -1, -2, -3
+SEG_NPTS = 21
+SEG_NSTATS = 12
+STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_pass", "lane_test1",
+              "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
+              "lane_sphere_tests", "ctas")
+
+
+class SegError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class seg_atlas_info(ctypes.Structure):
+    _fields_ = [("n_centroids", ctypes.c_int64), ("n_bundles", ctypes.c_int32),
+                ("n_tiles", ctypes.c_int32), ("tile_size", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+
+
+def _load() -> ctypes.CDLL:
+    path = _build.LIB
+    if _build.stale():
+        _build.build()          # compiles the CUDA library; raises if nvcc is unavailable
+    if not os.path.exists(path):
+        raise ImportError(f"libsegb200.so missing at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    lib.seg_create.restype = ctypes.c_int
+    lib.seg_create.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.seg_classify.restype = ctypes.c_int
+    lib.seg_classify.argtypes = [vp, vp, i64, vp, vp, vp]
+    lib.seg_classify_stats.restype = ctypes.c_int
+    lib.seg_classify_stats.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    lib.seg_get_atlas_info.restype = ctypes.c_int
+    lib.seg_get_atlas_info.argtypes = [vp, ctypes.POINTER(seg_atlas_info)]
+    lib.seg_plan_tiles.restype = ctypes.c_int
+    lib.seg_plan_tiles.argtypes = [vp, vp, i64, i32, i32, ctypes.POINTER(i32), vp, vp, vp]
+    lib.seg_profile_enable.restype = ctypes.c_int
+    lib.seg_profile_enable.argtypes = [vp, i32]
+    lib.seg_profile_read.restype = ctypes.c_int
+    lib.seg_profile_read.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    lib.seg_destroy.restype = None
+    lib.seg_destroy.argtypes = [vp]
+    lib.seg_last_error.restype = ctypes.c_char_p
+    lib.seg_last_error.argtypes = []
+    return lib
+
+
+LIB = _load()
+EXPORTS = ("seg_create", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
+           "seg_profile_enable", "seg_profile_read", "seg_destroy", "seg_last_error")
+
+
+def seg_last_error() -> str:
+    return LIB.seg_last_error().decode()
+
+
+def _check(rc: int) -> None:
+    if rc != SEG_OK:
+        raise SegError(rc, seg_last_error())
+
+
+def _ptr(x) -> int | None:
+    """Raw address of a torch tensor or numpy array (no copies, no dtype conversion)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def seg_create(centroids, bundle_id, M: int, thresh, B: int, device: int = -1) -> int:
+    """Returns an opaque seg_atlas handle (int).  Buffers: host or device, see seg.h."""
+    out = ctypes.c_void_p()
+    _check(LIB.seg_create(_ptr(centroids), _ptr(bundle_id), int(M), _ptr(thresh), int(B), int(device),
+                          ctypes.byref(out)))
+    return out.value
+
+
+def seg_classify(atlas: int, fibers, N: int, label, dist, stream: int | None = None) -> None:
+    _check(LIB.seg_classify(atlas, _ptr(fibers), int(N), _ptr(label), _ptr(dist), stream))
+
+
+def seg_classify_stats(atlas: int, fibers, N: int, label, dist, stats, stream: int | None = None) -> None:
+    _check(LIB.seg_classify_stats(atlas, _ptr(fibers), int(N), _ptr(label), _ptr(dist), _ptr(stats), stream))
+
+
+def seg_get_atlas_info(atlas: int) -> dict:
+    info = seg_atlas_info()
+    _check(LIB.seg_get_atlas_info(atlas, ctypes.byref(info)))
+    return {k: getattr(info, k) for k, _ in seg_atlas_info._fields_}
+
+
+def seg_plan_tiles(centroids, bundle_id, M: int, B: int, max_tiles: int, tile_bundle=None, tile_members=None,
+                   tile_spheres=None) -> int:
+    nt = ctypes.c_int32()
+    _check(LIB.seg_plan_tiles(_ptr(centroids), _ptr(bundle_id), int(M), int(B), int(max_tiles),
+                              ctypes.byref(nt), _ptr(tile_bundle), _ptr(tile_members), _ptr(tile_spheres)))
+    return nt.value
+
+
+def seg_profile_enable(atlas: int, capacity: int) -> None:
+    _check(LIB.seg_profile_enable(atlas, int(capacity)))
+
+
+def seg_profile_read(atlas: int, prepass_ms, classify_ms, capacity: int) -> int:
+    cnt = ctypes.c_int32()
+    _check(LIB.seg_profile_read(atlas, _ptr(prepass_ms), _ptr(classify_ms), int(capacity), ctypes.byref(cnt)))
+    return cnt.value
+
+
+def seg_destroy(atlas: int | None) -> None:
+    LIB.seg_destroy(atlas)

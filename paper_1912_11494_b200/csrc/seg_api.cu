@@ -1,0 +1,643 @@
+// seg_api.cu -- the C ABI of libsegb200.so (include/seg.h): argument validation, the
+// host-side atlas preparation, the device launch sequence and the
+// host-buffer streaming path.  Every step of the hot path runs in the kernels of classify.cu;
+// this file only plans, copies and launches.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/seg.h"
+#include "seg_internal.cuh"
+
+using namespace seg;
+
+// ----------------------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+static int cuda_fail(cudaError_t e, const char *what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();  // clear sticky-less error state
+    return fail(SEG_ECUDA, m);
+}
+#define SEG_CUDA(call, what)                          \
+    do {                                              \
+        cudaError_t e__ = (call);                     \
+        if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+    } while (0)
+
+extern "C" const char *seg_last_error(void) { return g_err.c_str(); }
+
+// ----------------------------------------------------------------------------------------
+// the atlas context
+// ----------------------------------------------------------------------------------------
+struct seg_atlas {
+    int device = 0;
+    int64_t M = 0;
+    int B = 0, T = 0;
+    float4 *tiles = nullptr;      // [T][21][32]
+    TileHdr *th = nullptr;        // [T]
+    BundleHdr *bh = nullptr;      // [B]
+    float3 lo{}, inv_cell{};      // Morton grid of the prepass
+    int64_t bytes = 0;
+    // profiling hook (seg_profile_enable / seg_profile_read); mutable, not thread-safe
+    mutable std::vector<cudaEvent_t> prof_ev;  // 3 per recorded call
+    mutable int prof_cap = 0, prof_n = 0;
+};
+
+namespace {
+
+struct DeviceGuard {  // restores the caller's current device
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); return; }
+        ok = (prev == dev) || cudaSetDevice(dev) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// 1 = device (or managed) memory, 0 = host memory, -1 = CUDA unavailable
+int pointer_kind(const void *p, int *dev) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        *dev = a.device;
+        return 1;
+    }
+    return 0;
+}
+
+// Tile plan (row a0): group by bundle, canonicalise each centroid's point order against the
+// bundle's first member (d_ME is invariant under reversing a centroid, Eq. 2, so this is
+// exact), split every bundle recursively at the median of its widest feature among
+// points 0/10/20 into tiles of 32, pad the last tile by repeating a real member (a duplicate
+// of a member of the same bundle can never change a (distance, bundle) minimum), and bound
+// points 0/10/20 of each tile by spheres (double precision, radius rounded up to FP32).
+struct Plan {
+    int T = 0;
+    std::vector<int> tile_bundle;           // [T]
+    std::vector<int> members;               // [T*32] caller centroid index
+    std::vector<unsigned char> flipped;     // [M] stored reversed?
+    std::vector<float> spheres;             // [T*12]
+    std::vector<int> b_t0, b_t1;            // [B]
+    std::vector<float> b_s10;               // [B*4]
+};
+
+void sphere(const float *cents, const std::vector<unsigned char> &flipped, const int *mem, int cnt, int point,
+            float out[4]) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    auto pt = [&](int m, int k) -> double {
+        const int pp = flipped[m] ? (NPTS - 1 - point) : point;
+        return (double)cents[(size_t)m * 3 * NPTS + 3 * pp + k];
+    };
+    for (int j = 0; j < cnt; ++j)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], pt(mem[j], k));
+            hi[k] = std::max(hi[k], pt(mem[j], k));
+        }
+    float c[3];
+    for (int k = 0; k < 3; ++k) c[k] = (float)(0.5 * (lo[k] + hi[k]));
+    double r2 = 0.0;
+    for (int j = 0; j < cnt; ++j) {
+        double s = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double d = pt(mem[j], k) - (double)c[k];
+            s += d * d;
+        }
+        r2 = std::max(r2, s);
+    }
+    const double r = std::sqrt(r2);
+    float rf = (float)r;
+    while ((double)rf < r) rf = std::nextafter(rf, INFINITY);
+    out[0] = c[0];
+    out[1] = c[1];
+    out[2] = c[2];
+    out[3] = rf;
+}
+
+void split_tiles(const float *cents, const std::vector<unsigned char> &flipped, std::vector<int> &ids, int lo,
+                 int hi, std::vector<std::vector<int>> &tiles_out) {
+    const int n = hi - lo;
+    if (n <= TILE) {
+        tiles_out.emplace_back(ids.begin() + lo, ids.begin() + hi);
+        return;
+    }
+    const int ntiles = (n + TILE - 1) / TILE;
+    const int left = (ntiles / 2) * TILE;
+    auto feat = [&](int m, int d) -> float {
+        const int point = (d / 3) == 0 ? 0 : ((d / 3) == 1 ? 10 : 20);
+        const int pp = flipped[m] ? (NPTS - 1 - point) : point;
+        return cents[(size_t)m * 3 * NPTS + 3 * pp + (d % 3)];
+    };
+    int best_d = 0;
+    float best_ext = -1.f;
+    for (int d = 0; d < 9; ++d) {
+        float mn = INFINITY, mx = -INFINITY;
+        for (int j = lo; j < hi; ++j) {
+            const float v = feat(ids[j], d);
+            mn = std::min(mn, v);
+            mx = std::max(mx, v);
+        }
+        if (mx - mn > best_ext) {
+            best_ext = mx - mn;
+            best_d = d;
+        }
+    }
+    std::nth_element(ids.begin() + lo, ids.begin() + lo + left, ids.begin() + hi, [&](int a, int b) {
+        const float fa = feat(a, best_d), fb = feat(b, best_d);
+        return fa < fb || (fa == fb && a < b);
+    });
+    split_tiles(cents, flipped, ids, lo, lo + left, tiles_out);
+    split_tiles(cents, flipped, ids, lo + left, hi, tiles_out);
+}
+
+int make_plan(const float *cents, const int32_t *bid, int64_t M, int B, Plan &P) {
+    try {
+        std::vector<std::vector<int>> by_b(B);
+        for (int64_t m = 0; m < M; ++m) by_b[bid[m]].push_back((int)m);
+        P.flipped.assign(M, 0);
+        auto at = [&](int m, int point, int k) { return (double)cents[(size_t)m * 3 * NPTS + 3 * point + k]; };
+        for (int b = 0; b < B; ++b) {
+            if (by_b[b].empty()) continue;
+            const int r = by_b[b][0];
+            for (int m : by_b[b]) {
+                double same = 0, rev = 0;
+                for (int k = 0; k < 3; ++k) {
+                    const double a0 = at(m, 0, k) - at(r, 0, k), a1 = at(m, 20, k) - at(r, 20, k);
+                    const double b0 = at(m, 20, k) - at(r, 0, k), b1 = at(m, 0, k) - at(r, 20, k);
+                    same += a0 * a0 + a1 * a1;
+                    rev += b0 * b0 + b1 * b1;
+                }
+                P.flipped[m] = rev < same ? 1 : 0;
+            }
+        }
+        P.b_t0.assign(B, 0);
+        P.b_t1.assign(B, 0);
+        P.b_s10.assign((size_t)B * 4, 0.f);
+        P.T = 0;
+        P.tile_bundle.clear();
+        P.members.clear();
+        P.spheres.clear();
+        for (int b = 0; b < B; ++b) {
+            P.b_t0[b] = P.T;
+            if (by_b[b].empty()) {
+                P.b_t1[b] = P.T;
+                continue;
+            }
+            std::vector<std::vector<int>> tl;
+            split_tiles(cents, P.flipped, by_b[b], 0, (int)by_b[b].size(), tl);
+            for (auto &t : tl) {
+                std::sort(t.begin(), t.end());
+                P.tile_bundle.push_back(b);
+                for (int k = 0; k < TILE; ++k) P.members.push_back(t[std::min<int>(k, (int)t.size() - 1)]);
+                float s[4];
+                for (int q = 0; q < 3; ++q) {
+                    sphere(cents, P.flipped, t.data(), (int)t.size(), q == 0 ? 0 : (q == 1 ? 10 : 20), s);
+                    for (int k = 0; k < 4; ++k) P.spheres.push_back(s[k]);
+                }
+                ++P.T;
+            }
+            P.b_t1[b] = P.T;
+            sphere(cents, P.flipped, by_b[b].data(), (int)by_b[b].size(), 10, &P.b_s10[(size_t)b * 4]);
+        }
+    } catch (const std::bad_alloc &) {
+        return fail(SEG_ENOMEM, "seg_create: host allocation failed");
+    }
+    return SEG_OK;
+}
+
+int validate_atlas_host(const float *cents, const int32_t *bid, int64_t M, const float *thr, int B) {
+    for (int64_t m = 0; m < M; ++m)
+        if (bid[m] < 0 || bid[m] >= B)
+            return fail(SEG_EINVAL, "seg_create: bundle_id[" + std::to_string(m) + "] = " +
+                                        std::to_string(bid[m]) + " not in [0, B)");
+    for (size_t i = 0; i < (size_t)M * 3 * NPTS; ++i)
+        if (!std::isfinite(cents[i]))
+            return fail(SEG_EINVAL, "seg_create: non-finite centroid coordinate at flat index " + std::to_string(i));
+    if (thr)
+        for (int b = 0; b < B; ++b)
+            if (!std::isfinite(thr[b]) || !(thr[b] > 0.f))
+                return fail(SEG_EINVAL, "seg_create: thresh[" + std::to_string(b) + "] must be finite and > 0");
+    return SEG_OK;
+}
+
+// Stage a caller array (host or device) into a host vector.
+template <class T>
+int to_host(const T *p, size_t n, std::vector<T> &out, int *dev_seen) {
+    int dev = -1;
+    const int kind = pointer_kind(p, &dev);
+    try {
+        out.resize(n);
+    } catch (const std::bad_alloc &) {
+        return fail(SEG_ENOMEM, "seg_create: host allocation failed");
+    }
+    if (kind == 1) {
+        *dev_seen = dev;
+        SEG_CUDA(cudaMemcpy(out.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), "seg_create: cudaMemcpy D2H");
+    } else if (kind == 0) {
+        std::memcpy(out.data(), p, n * sizeof(T));
+    } else {
+        return fail(SEG_ECUDA, "seg_create: no usable CUDA device");
+    }
+    return SEG_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------------------
+// seg_plan_tiles (host only)
+// ----------------------------------------------------------------------------------------
+extern "C" int seg_plan_tiles(const float *centroids, const int32_t *bundle_id, int64_t M, int32_t B,
+                              int32_t max_tiles, int32_t *n_tiles, int32_t *tile_bundle, int32_t *tile_members,
+                              float *tile_spheres) {
+    if (!centroids || !bundle_id || !n_tiles) return fail(SEG_EINVAL, "seg_plan_tiles: null pointer");
+    if (M < 1 || M > INT32_MAX || B < 1) return fail(SEG_EINVAL, "seg_plan_tiles: M and B must be >= 1");
+    int rc = validate_atlas_host(centroids, bundle_id, M, nullptr, B);
+    if (rc) return rc;
+    Plan P;
+    rc = make_plan(centroids, bundle_id, M, B, P);
+    if (rc) return rc;
+    *n_tiles = P.T;
+    const int nt = std::min(P.T, std::max(0, max_tiles));
+    for (int t = 0; t < nt; ++t) {
+        if (tile_bundle) tile_bundle[t] = P.tile_bundle[t];
+        if (tile_members)
+            for (int k = 0; k < TILE; ++k) tile_members[t * TILE + k] = P.members[(size_t)t * TILE + k];
+        if (tile_spheres)
+            for (int k = 0; k < 12; ++k) tile_spheres[t * 12 + k] = P.spheres[(size_t)t * 12 + k];
+    }
+    g_err.clear();
+    return SEG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// seg_create / seg_destroy / seg_get_atlas_info
+// ----------------------------------------------------------------------------------------
+static void free_prof(const seg_atlas *a) {
+    for (cudaEvent_t e : a->prof_ev) cudaEventDestroy(e);
+    a->prof_ev.clear();
+    a->prof_cap = a->prof_n = 0;
+}
+
+static void free_atlas(seg_atlas *a) {
+    if (!a) return;
+    DeviceGuard g(a->device);
+    free_prof(a);
+    cudaFree(a->tiles);
+    cudaFree(a->th);
+    cudaFree(a->bh);
+    delete a;
+}
+
+extern "C" void seg_destroy(seg_atlas *a) { free_atlas(a); }
+
+extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M, const float *thresh,
+                          int32_t B, int device, seg_atlas **out) {
+    if (out) *out = nullptr;
+    if (!centroids || !bundle_id || !thresh || !out) return fail(SEG_EINVAL, "seg_create: null pointer");
+    if (M < 1 || M > INT32_MAX) return fail(SEG_EINVAL, "seg_create: M must be in [1, 2^31-1]");
+    if (B < 1) return fail(SEG_EINVAL, "seg_create: B must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        return fail(SEG_ECUDA, "seg_create: no usable CUDA device");
+    }
+    if (device < 0) SEG_CUDA(cudaGetDevice(&device), "seg_create: cudaGetDevice");
+    if (device >= ndev) return fail(SEG_EINVAL, "seg_create: device ordinal out of range");
+    DeviceGuard guard(device);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_create: cudaSetDevice failed");
+
+    std::vector<float> cents, thr;
+    std::vector<int32_t> bid;
+    int dev_seen = device;
+    int rc = to_host(centroids, (size_t)M * 3 * NPTS, cents, &dev_seen);
+    if (!rc) rc = to_host(bundle_id, (size_t)M, bid, &dev_seen);
+    if (!rc) rc = to_host(thresh, (size_t)B, thr, &dev_seen);
+    if (rc) return rc;
+    rc = validate_atlas_host(cents.data(), bid.data(), M, thr.data(), B);
+    if (rc) return rc;
+    Plan P;
+    rc = make_plan(cents.data(), bid.data(), M, B, P);
+    if (rc) return rc;
+
+    // device images
+    std::vector<float4> tiles((size_t)P.T * TILE_F4);
+    std::vector<TileHdr> th(P.T);
+    std::vector<BundleHdr> bh(B);
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int t = 0; t < P.T; ++t) {
+        for (int k = 0; k < TILE; ++k) {
+            const int m = P.members[(size_t)t * TILE + k];
+            for (int i = 0; i < NPTS; ++i) {
+                const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
+                const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
+                tiles[((size_t)t * NPTS + i) * TILE + k] = make_float4(c[0], c[1], c[2], 0.f);
+                for (int d = 0; d < 3; ++d) {
+                    lo[d] = std::min(lo[d], c[d]);
+                    hi[d] = std::max(hi[d], c[d]);
+                }
+            }
+        }
+        const float *s = &P.spheres[(size_t)t * 12];
+        const int b = P.tile_bundle[t];
+        th[t].s0 = make_float4(s[0], s[1], s[2], s[3]);
+        th[t].s10 = make_float4(s[4], s[5], s[6], s[7]);
+        th[t].s20 = make_float4(s[8], s[9], s[10], s[11]);
+        th[t].bundle = b;
+        th[t].thr = thr[b];
+        th[t].thr2 = thr[b] * thr[b];
+        th[t].pad = 0;
+    }
+    float maxthr = 0.f;
+    for (int b = 0; b < B; ++b) {
+        const float *s = &P.b_s10[(size_t)b * 4];
+        bh[b].s10 = make_float4(s[0], s[1], s[2], s[3]);
+        bh[b].t0 = P.b_t0[b];
+        bh[b].t1 = P.b_t1[b];
+        bh[b].thr = thr[b];
+        bh[b].thr2 = thr[b] * thr[b];
+        maxthr = std::max(maxthr, thr[b]);
+    }
+
+    seg_atlas *a = new (std::nothrow) seg_atlas();
+    if (!a) return fail(SEG_ENOMEM, "seg_create: host allocation failed");
+    a->device = device;
+    a->M = M;
+    a->B = B;
+    a->T = P.T;
+    float ext[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] -= maxthr;
+        hi[d] += maxthr;
+        ext[d] = std::max(hi[d] - lo[d], 1e-3f);
+    }
+    const float nb = (float)(1 << MORTON_BITS);
+    a->lo = make_float3(lo[0], lo[1], lo[2]);
+    a->inv_cell = make_float3(nb / ext[0], nb / ext[1], nb / ext[2]);
+    const size_t bt = tiles.size() * sizeof(float4), bth = th.size() * sizeof(TileHdr),
+                 bbh = bh.size() * sizeof(BundleHdr);
+    cudaError_t e = cudaMalloc(&a->tiles, bt);
+    if (e == cudaSuccess) e = cudaMalloc(&a->th, bth);
+    if (e == cudaSuccess) e = cudaMalloc(&a->bh, bbh);
+    if (e != cudaSuccess) {
+        free_atlas(a);
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? SEG_ENOMEM : SEG_ECUDA,
+                    std::string("seg_create: cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    e = cudaMemcpy(a->tiles, tiles.data(), bt, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(a->th, th.data(), bth, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(a->bh, bh.data(), bbh, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        free_atlas(a);
+        return cuda_fail(e, "seg_create: cudaMemcpy H2D");
+    }
+    a->bytes = (int64_t)(bt + bth + bbh);
+    // keep stream-ordered scratch cached between seg_classify calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr_bytes = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr_bytes);
+    }
+    cudaGetLastError();
+    *out = a;
+    g_err.clear();
+    return SEG_OK;
+}
+
+extern "C" int seg_get_atlas_info(const seg_atlas *a, seg_atlas_info *info) {
+    if (!a || !info) return fail(SEG_EINVAL, "seg_get_atlas_info: null pointer");
+    info->n_centroids = a->M;
+    info->n_bundles = a->B;
+    info->n_tiles = a->T;
+    info->tile_size = TILE;
+    info->device = a->device;
+    info->device_bytes = a->bytes;
+    return SEG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// seg_classify
+// ----------------------------------------------------------------------------------------
+namespace {
+
+constexpr int SORT_MIN_N = 4096;   // below this the prepass costs more than it saves
+
+// Device pointers, asynchronous on s.
+int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, float *dist, cudaStream_t s,
+                    unsigned long long *d_stats) {
+    if (n == 0) return SEG_OK;
+    cudaEvent_t *ev = nullptr;
+    if (a->prof_n < a->prof_cap) ev = &a->prof_ev[3 * (a->prof_n++)];
+    if (ev) SEG_CUDA(cudaEventRecord(ev[0], s), "seg_classify: profile event");
+    uint32_t *key = nullptr, *hist = nullptr;
+    int32_t *perm = nullptr;
+    if (n >= SORT_MIN_N) {
+        SEG_CUDA(cudaMallocAsync((void **)&key, sizeof(uint32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
+        SEG_CUDA(cudaMallocAsync((void **)&perm, sizeof(int32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
+        SEG_CUDA(cudaMallocAsync((void **)&hist, sizeof(uint32_t) * MORTON_BUCKETS, s),
+                 "seg_classify: cudaMallocAsync");
+        MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, perm};
+        SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
+    }
+    ClassifyParams cp{fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats};
+    if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
+    cudaError_t e = launch_classify(cp, d_stats != nullptr, s);
+    if (ev && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
+    if (key) {
+        cudaFreeAsync(key, s);
+        cudaFreeAsync(perm, s);
+        cudaFreeAsync(hist, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "seg_classify: kernel launch");
+    return SEG_OK;
+}
+
+// Host pointers: chunked H2D -> classify -> D2H, double-buffered over two streams.
+int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab, float *dist, cudaStream_t s) {
+    constexpr int64_t CH = 1 << 19;  // fibers per chunk (126 MB)
+    const int64_t nchunks = (N + CH - 1) / CH;
+    const int nb = nchunks > 1 ? 2 : 1;
+    const int64_t cap = std::min<int64_t>(N, CH);
+    cudaStream_t cs = nullptr;
+    SEG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "seg_classify: cudaStreamCreate");
+    cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
+    float *dfib[2] = {};
+    int32_t *dlab[2] = {};
+    float *ddist[2] = {};
+    int rc = SEG_OK;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < nb && e == cudaSuccess; ++i) {
+        e = cudaMallocAsync((void **)&dfib[i], sizeof(float) * 3 * NPTS * cap, s);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&dlab[i], sizeof(int32_t) * cap, s);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&ddist[i], sizeof(float) * cap, s);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
+    }
+    // the copy stream must see the allocations made on s
+    cudaEvent_t ev_alloc = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_alloc, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_alloc, 0);
+    for (int64_t c = 0; c < nchunks && e == cudaSuccess && rc == SEG_OK; ++c) {
+        const int i = (int)(c % nb);
+        const int64_t lo = c * CH, n = std::min(CH, N - lo);
+        if (c >= nb) e = cudaStreamWaitEvent(cs, ev_out[i], 0);  // buffer i free (its D2H done)
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dfib[i], fib + lo * 3 * NPTS, sizeof(float) * 3 * NPTS * n, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in[i], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in[i], 0);
+        if (e != cudaSuccess) break;
+        rc = classify_device(a, dfib[i], (int)n, dlab[i], ddist[i], s, nullptr);
+        if (rc) break;
+        e = cudaEventRecord(ev_done[i], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_done[i], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(lab + lo, dlab[i], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dist + lo, ddist[i], sizeof(float) * n, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_out[i], cs);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = e2;
+    // the frees are ordered after the last copies on s
+    cudaEvent_t ev_fin = nullptr;
+    if (cudaEventCreateWithFlags(&ev_fin, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(ev_fin, cs);
+        cudaStreamWaitEvent(s, ev_fin, 0);
+    }
+    for (int i = 0; i < nb; ++i) {
+        if (dfib[i]) cudaFreeAsync(dfib[i], s);
+        if (dlab[i]) cudaFreeAsync(dlab[i], s);
+        if (ddist[i]) cudaFreeAsync(ddist[i], s);
+        if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+        if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+        if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+    }
+    e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+    if (ev_alloc) cudaEventDestroy(ev_alloc);
+    if (ev_fin) cudaEventDestroy(ev_fin);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "seg_classify: host-buffer pipeline");
+    return SEG_OK;
+}
+
+int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t *label, float *dist, void *stream,
+                    uint64_t *stats) {
+    if (!a) return fail(SEG_EINVAL, "seg_classify: null atlas");
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_classify: N must be in [0, 2^31-1]");
+    if (N == 0) {
+        g_err.clear();
+        return SEG_OK;
+    }
+    if (!fibers || !label || !dist) return fail(SEG_EINVAL, "seg_classify: null pointer with N > 0");
+    if (((uintptr_t)fibers & 3) || ((uintptr_t)label & 3) || ((uintptr_t)dist & 3))
+        return fail(SEG_EINVAL, "seg_classify: pointers must be 4-byte aligned");
+    int d0 = -1, d1 = -1, d2 = -1;
+    const int k0 = pointer_kind(fibers, &d0), k1 = pointer_kind(label, &d1), k2 = pointer_kind(dist, &d2);
+    if (k0 < 0 || k1 < 0 || k2 < 0) return fail(SEG_ECUDA, "seg_classify: no usable CUDA device");
+    if (k0 != k1 || k0 != k2) return fail(SEG_EINVAL, "seg_classify: fibers/label/dist mix host and device memory");
+    if (k0 == 1 && (d0 != a->device || d1 != a->device || d2 != a->device))
+        return fail(SEG_EINVAL, "seg_classify: device pointer not on the atlas's device");
+    DeviceGuard guard(a->device);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_classify: cudaSetDevice failed");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (k0 == 0) {
+        if (stats) return fail(SEG_EINVAL, "seg_classify_stats: device pointers only");
+        const int rc = classify_host(a, fibers, N, label, dist, s);
+        if (!rc) g_err.clear();
+        return rc;
+    }
+    unsigned long long *d_stats = nullptr;
+    if (stats) {
+        SEG_CUDA(cudaMallocAsync((void **)&d_stats, sizeof(unsigned long long) * SEG_NSTATS, s),
+                 "seg_classify_stats: cudaMallocAsync");
+        SEG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * SEG_NSTATS, s),
+                 "seg_classify_stats: memset");
+    }
+    int rc = classify_device(a, fibers, (int)N, label, dist, s, d_stats);
+    if (stats) {
+        unsigned long long h[SEG_NSTATS];
+        cudaError_t e = cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFreeAsync(d_stats, s);
+        if (!rc && e != cudaSuccess) return cuda_fail(e, "seg_classify_stats: readback");
+        for (int k = 0; k < SEG_NSTATS; ++k) stats[k] += h[k];
+    }
+    if (!rc) g_err.clear();
+    return rc;
+}
+
+}  // namespace
+
+extern "C" int seg_classify(const seg_atlas *a, const float *fibers, int64_t N, int32_t *label, float *dist,
+                            void *stream) {
+    return classify_common(a, fibers, N, label, dist, stream, nullptr);
+}
+
+extern "C" int seg_classify_stats(const seg_atlas *a, const float *fibers, int64_t N, int32_t *label, float *dist,
+                                  uint64_t *stats, void *stream) {
+    if (!stats) return fail(SEG_EINVAL, "seg_classify_stats: null stats");
+    return classify_common(a, fibers, N, label, dist, stream, stats);
+}
+
+extern "C" int seg_profile_enable(seg_atlas *a, int32_t cap) {
+    if (!a || cap < 0) return fail(SEG_EINVAL, "seg_profile_enable: null atlas or negative capacity");
+    DeviceGuard guard(a->device);
+    free_prof(a);
+    if (cap == 0) return SEG_OK;
+    try {
+        a->prof_ev.resize((size_t)3 * cap);
+    } catch (const std::bad_alloc &) {
+        return fail(SEG_ENOMEM, "seg_profile_enable: host allocation failed");
+    }
+    for (auto &e : a->prof_ev) {
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) {
+            e = nullptr;
+            free_prof(a);
+            return cuda_fail(r, "seg_profile_enable: cudaEventCreate");
+        }
+    }
+    a->prof_cap = cap;
+    a->prof_n = 0;
+    return SEG_OK;
+}
+
+extern "C" int seg_profile_read(seg_atlas *a, float *prepass_ms, float *classify_ms, int32_t cap, int32_t *count) {
+    if (!a || !count) return fail(SEG_EINVAL, "seg_profile_read: null pointer");
+    DeviceGuard guard(a->device);
+    *count = a->prof_n;
+    const int n = std::min(a->prof_n, std::max(0, (int)cap));
+    for (int i = 0; i < n; ++i) {
+        cudaEvent_t *ev = &a->prof_ev[3 * i];
+        SEG_CUDA(cudaEventSynchronize(ev[2]), "seg_profile_read: cudaEventSynchronize");
+        float t0 = 0.f, t1 = 0.f;
+        SEG_CUDA(cudaEventElapsedTime(&t0, ev[0], ev[1]), "seg_profile_read: elapsed");
+        SEG_CUDA(cudaEventElapsedTime(&t1, ev[1], ev[2]), "seg_profile_read: elapsed");
+        if (prepass_ms) prepass_ms[i] = t0;
+        if (classify_ms) classify_ms[i] = t1;
+    }
+    return SEG_OK;
+}

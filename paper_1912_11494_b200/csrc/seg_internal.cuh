@@ -1,0 +1,66 @@
+// seg_internal.cuh -- device data layout shared by the C-ABI layer (seg_api.cu) and the
+// sm_100a kernels (classify.cu).  Product code only; the oracle never includes it.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace seg {
+
+constexpr int NPTS = 21;                 // points per fiber / centroid
+constexpr int TILE = 32;                 // centroids per tile (one bit per centroid in a u32 mask)
+constexpr int TILE_F4 = NPTS * TILE;     // float4 per tile: [21 points][32 centroids]
+constexpr int TILE_BYTES = TILE_F4 * 16; // 10,752 B -> one 1-D TMA bulk copy
+constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
+constexpr int MORTON_BITS = 6;           // per axis -> 2^18 spatial buckets for the prepass
+constexpr int MORTON_BUCKETS = 1 << (3 * MORTON_BITS);
+
+// Per-tile header: bounding spheres (centre xyz, radius w) of centroid points 0, 10, 20
+// over the tile's members, the tile's bundle and its threshold (squared, FP32).
+struct __align__(16) TileHdr {
+    float4 s0, s10, s20;
+    int bundle;
+    float thr2;
+    float thr;
+    int pad;
+};
+static_assert(sizeof(TileHdr) == 64, "TileHdr is 64 B");
+
+// Per-bundle header: bounding sphere of point 10 over the bundle, tile range [t0, t1).
+struct __align__(16) BundleHdr {
+    float4 s10;
+    int t0, t1;
+    float thr;
+    float thr2;
+};
+static_assert(sizeof(BundleHdr) == 32, "BundleHdr is 32 B");
+
+struct ClassifyParams {
+    const float *fibers;      // [n][21][3]
+    int n;
+    const int32_t *perm;      // nullable: processing order -> caller index
+    int32_t *label;           // [n]
+    float *dist;              // [n]
+    const float4 *tiles;      // [T][21][32]
+    const TileHdr *th;        // [T]
+    const BundleHdr *bh;      // [B]
+    int B, T;
+    unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
+};
+
+struct MortonParams {
+    const float *fibers;
+    int n;
+    float3 lo;
+    float3 inv_cell;          // buckets per mm along each axis
+    uint32_t *key;            // [n]
+    uint32_t *hist;           // [MORTON_BUCKETS]
+    int32_t *perm;            // [n]
+};
+
+// Launchers (classify.cu).  All are asynchronous on `s`.
+cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
+cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s);
+size_t classify_smem_bytes(int B, int T);
+int classify_fibers_per_cta();
+
+}  // namespace seg

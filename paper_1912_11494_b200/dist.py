@@ -1,0 +1,64 @@
+"""Multi-GPU driver: one process per GPU, torch.distributed over NCCL.
+
+Fibers are independent units (Alg. 1's outer loop "has no collision problems",
+PAPER.md:152), so the data path needs no collective: each rank classifies its own
+contiguous shard.  The only exchanges are
+  * the atlas, replicated once at setup by a broadcast from rank 0 (C1), and
+  * optionally the labels, gathered after the classification (C2).
+Shard boundaries are multiples of 4 fibers so every shard starts 16-byte aligned.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of rank `rank`; chunk = 4 * ceil(n / (4 world))."""
+    chunk = 4 * (-(-n // (4 * world))) if n else 0
+    lo = min(n, rank * chunk)
+    return lo, min(n, lo + chunk)
+
+
+def broadcast_atlas(at, M: int, B: int, device, world: int):
+    """Replicate (centroids f32[M,21,3], bundle_id i32[M], thresh f32[B]) from rank 0 (C1).
+
+    `at` (a synth.Atlas or any object with .centroids/.bundle_id/.thresh numpy arrays) is
+    only needed on rank 0.  Returns tensors on `device`.
+    """
+    if at is not None:
+        c = torch.from_numpy(at.centroids).to(device)
+        b = torch.from_numpy(at.bundle_id).to(device)
+        t = torch.from_numpy(at.thresh).to(device)
+    else:
+        c = torch.empty((M, 21, 3), dtype=torch.float32, device=device)
+        b = torch.empty(M, dtype=torch.int32, device=device)
+        t = torch.empty(B, dtype=torch.float32, device=device)
+    if world > 1:
+        for x in (c, b, t):
+            dist.broadcast(x, src=0)
+    return c, b, t
+
+
+def classify_sharded(classify, fibers: torch.Tensor, n_total: int, world: int, rank: int,
+                     gather: bool = True):
+    """Strong-scaling path for one subject: this rank labels its shard `fibers`
+    (= fibers[shard_range(n_total, world, rank)]) with `classify(fibers) -> (label, dist)`,
+    then (gather=True) the padded shards are all-gathered (C2).  Returns the full
+    (label, dist) on every rank, or this rank's shard when gather=False."""
+    lab, dst = classify(fibers)
+    if not gather or world == 1:
+        return lab, dst
+    lo, hi = shard_range(n_total, world, rank)
+    chunk = shard_range(n_total, world, 0)[1]
+    packed = torch.full((chunk, 2), -1, dtype=torch.int32, device=lab.device)
+    packed[: hi - lo, 0] = lab
+    packed[: hi - lo, 1] = dst.view(torch.int32)
+    out = torch.empty((world * chunk, 2), dtype=torch.int32, device=lab.device)
+    dist.all_gather_into_tensor(out, packed)
+    rows = []
+    for r in range(world):
+        a, b = shard_range(n_total, world, r)
+        rows.append(out[r * chunk: r * chunk + (b - a)])
+    full = torch.cat(rows)
+    return full[:, 0].contiguous(), full[:, 1].contiguous().view(torch.float32)
