@@ -152,6 +152,17 @@ int seg_profile_enable(seg_atlas *atlas, int32_t capacity);
 int seg_profile_read(seg_atlas *atlas, float *prepass_ms, float *classify_ms, int32_t capacity,
                      int32_t *count);
 
+/*
+ * seg_debug_classify_seeded -- experiment hook (device pointers only): seg_classify with each
+ * fiber's running best initialised from seed_keys[N] (device uint64, caller order), key =
+ * (float bits of a squared distance << 32) | bundle id, or ~0 for none.  The result equals
+ * seg_classify's whenever every seed is an upper bound of the fiber's true best key, e.g.
+ * (d^2 rounded up, label) from an earlier run; it measures how much of the kernel's work a
+ * perfect best-first order would save.  Errors as seg_classify.
+ */
+int seg_debug_classify_seeded(const seg_atlas *atlas, const float *fibers, int64_t N,
+                              const uint64_t *seed_keys, int32_t *label, float *dist, void *stream);
+
 /* Destroy a context (NULL-safe).  Must not race an in-flight seg_classify. */
 void seg_destroy(seg_atlas *atlas);
 

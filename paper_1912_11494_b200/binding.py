@@ -49,6 +49,8 @@ def _load() -> ctypes.CDLL:
     lib.seg_get_atlas_info.argtypes = [vp, ctypes.POINTER(seg_atlas_info)]
     lib.seg_plan_tiles.restype = ctypes.c_int
     lib.seg_plan_tiles.argtypes = [vp, vp, i64, i32, i32, ctypes.POINTER(i32), vp, vp, vp]
+    lib.seg_debug_classify_seeded.restype = ctypes.c_int
+    lib.seg_debug_classify_seeded.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     lib.seg_profile_enable.restype = ctypes.c_int
     lib.seg_profile_enable.argtypes = [vp, i32]
     lib.seg_profile_read.restype = ctypes.c_int
@@ -62,7 +64,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTS = ("seg_create", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
-           "seg_profile_enable", "seg_profile_read", "seg_destroy", "seg_last_error")
+           "seg_profile_enable", "seg_profile_read", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
 
 
 def seg_last_error() -> str:
@@ -115,6 +117,10 @@ def seg_plan_tiles(centroids, bundle_id, M: int, B: int, max_tiles: int, tile_bu
     _check(LIB.seg_plan_tiles(_ptr(centroids), _ptr(bundle_id), int(M), int(B), int(max_tiles),
                               ctypes.byref(nt), _ptr(tile_bundle), _ptr(tile_members), _ptr(tile_spheres)))
     return nt.value
+
+
+def seg_debug_classify_seeded(atlas: int, fibers, N: int, seed_keys, label, dist, stream: int | None = None) -> None:
+    _check(LIB.seg_debug_classify_seeded(atlas, _ptr(fibers), int(N), _ptr(seed_keys), _ptr(label), _ptr(dist), stream))
 
 
 def seg_profile_enable(atlas: int, capacity: int) -> None:

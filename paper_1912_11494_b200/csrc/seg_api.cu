@@ -45,7 +45,7 @@ struct seg_atlas {
     int device = 0;
     int64_t M = 0;
     int B = 0, T = 0;
-    float4 *tiles = nullptr;      // [T][21][32]
+    float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points
     TileHdr *th = nullptr;        // [T]
     BundleHdr *bh = nullptr;      // [B]
     float3 lo{}, inv_cell{};      // Morton grid of the prepass
@@ -339,7 +339,7 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
     if (rc) return rc;
 
     // device images
-    std::vector<float4> tiles((size_t)P.T * TILE_F4);
+    std::vector<float4> tiles((size_t)P.T * TILE_STRIDE_F4);
     std::vector<TileHdr> th(P.T);
     std::vector<BundleHdr> bh(B);
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -349,7 +349,8 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
             for (int i = 0; i < NPTS; ++i) {
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
-                tiles[((size_t)t * NPTS + i) * TILE + k] = make_float4(c[0], c[1], c[2], 0.f);
+                tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] =
+                    make_float4(c[0], c[1], c[2], 0.f);
                 for (int d = 0; d < 3; ++d) {
                     lo[d] = std::min(lo[d], c[d]);
                     hi[d] = std::max(hi[d], c[d]);
@@ -365,6 +366,7 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
         th[t].thr = thr[b];
         th[t].thr2 = thr[b] * thr[b];
         th[t].pad = 0;
+        std::memcpy(&tiles[(size_t)t * TILE_STRIDE_F4], &th[t], sizeof(TileHdr));
     }
     float maxthr = 0.f;
     for (int b = 0; b < B; ++b) {
@@ -443,7 +445,7 @@ constexpr int SORT_MIN_N = 4096;   // below this the prepass costs more than it 
 
 // Device pointers, asynchronous on s.
 int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, float *dist, cudaStream_t s,
-                    unsigned long long *d_stats) {
+                    unsigned long long *d_stats, const unsigned long long *seed = nullptr) {
     if (n == 0) return SEG_OK;
     cudaEvent_t *ev = nullptr;
     if (a->prof_n < a->prof_cap) ev = &a->prof_ev[3 * (a->prof_n++)];
@@ -458,7 +460,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
         MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, perm};
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
-    ClassifyParams cp{fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats};
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
@@ -544,7 +546,7 @@ int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab,
 }
 
 int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t *label, float *dist, void *stream,
-                    uint64_t *stats) {
+                    uint64_t *stats, const uint64_t *seed = nullptr) {
     if (!a) return fail(SEG_EINVAL, "seg_classify: null atlas");
     if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_classify: N must be in [0, 2^31-1]");
     if (N == 0) {
@@ -564,7 +566,7 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
     if (!guard.ok) return fail(SEG_ECUDA, "seg_classify: cudaSetDevice failed");
     cudaStream_t s = (cudaStream_t)stream;
     if (k0 == 0) {
-        if (stats) return fail(SEG_EINVAL, "seg_classify_stats: device pointers only");
+        if (stats || seed) return fail(SEG_EINVAL, "seg_classify_stats / seeded: device pointers only");
         const int rc = classify_host(a, fibers, N, label, dist, s);
         if (!rc) g_err.clear();
         return rc;
@@ -576,7 +578,8 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
         SEG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * SEG_NSTATS, s),
                  "seg_classify_stats: memset");
     }
-    int rc = classify_device(a, fibers, (int)N, label, dist, s, d_stats);
+    int rc = classify_device(a, fibers, (int)N, label, dist, s, d_stats,
+                             reinterpret_cast<const unsigned long long *>(seed));
     if (stats) {
         unsigned long long h[SEG_NSTATS];
         cudaError_t e = cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -640,4 +643,10 @@ extern "C" int seg_profile_read(seg_atlas *a, float *prepass_ms, float *classify
         if (classify_ms) classify_ms[i] = t1;
     }
     return SEG_OK;
+}
+
+extern "C" int seg_debug_classify_seeded(const seg_atlas *a, const float *fibers, int64_t N, const uint64_t *seed,
+                                         int32_t *label, float *dist, void *stream) {
+    if (!seed && N > 0) return fail(SEG_EINVAL, "seg_debug_classify_seeded: null seed_keys");
+    return classify_common(a, fibers, N, label, dist, stream, nullptr, seed);
 }

@@ -8,8 +8,10 @@ namespace seg {
 
 constexpr int NPTS = 21;                 // points per fiber / centroid
 constexpr int TILE = 32;                 // centroids per tile (one bit per centroid in a u32 mask)
-constexpr int TILE_F4 = NPTS * TILE;     // float4 per tile: [21 points][32 centroids]
-constexpr int TILE_BYTES = TILE_F4 * 16; // 10,752 B -> one 1-D TMA bulk copy
+constexpr int TILE_F4 = NPTS * TILE;     // float4 of tile point data: [21 points][32 centroids]
+constexpr int TILE_HDR_F4 = 4;           // the tile's 64-B TileHdr travels in front of its data
+constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
+constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,816 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
 constexpr int MORTON_BITS = 6;           // per axis -> 2^18 spatial buckets for the prepass
 constexpr int MORTON_BUCKETS = 1 << (3 * MORTON_BITS);
@@ -35,12 +37,13 @@ struct __align__(16) BundleHdr {
 static_assert(sizeof(BundleHdr) == 32, "BundleHdr is 32 B");
 
 struct ClassifyParams {
+    const unsigned long long *seed;  // nullable [n] initial best keys (d2 bits << 32 | bundle), by caller index
     const float *fibers;      // [n][21][3]
     int n;
     const int32_t *perm;      // nullable: processing order -> caller index
     int32_t *label;           // [n]
     float *dist;              // [n]
-    const float4 *tiles;      // [T][21][32]
+    const float4 *tiles;      // [T][TILE_STRIDE_F4]: TileHdr, then [21][32] points
     const TileHdr *th;        // [T]
     const BundleHdr *bh;      // [B]
     int B, T;
