@@ -161,7 +161,8 @@ int seg_profile_read(seg_atlas *atlas, float *prepass_ms, float *classify_ms, in
  * perfect best-first order would save.  Errors as seg_classify.
  */
 int seg_debug_classify_seeded(const seg_atlas *atlas, const float *fibers, int64_t N,
-                              const uint64_t *seed_keys, int32_t *label, float *dist, void *stream);
+                              const uint64_t *seed_keys, int32_t *label, float *dist,
+                              uint64_t *stats /* nullable host [SEG_NSTATS] */, void *stream);
 
 /* Destroy a context (NULL-safe).  Must not race an in-flight seg_classify. */
 void seg_destroy(seg_atlas *atlas);

@@ -50,7 +50,7 @@ def _load() -> ctypes.CDLL:
     lib.seg_plan_tiles.restype = ctypes.c_int
     lib.seg_plan_tiles.argtypes = [vp, vp, i64, i32, i32, ctypes.POINTER(i32), vp, vp, vp]
     lib.seg_debug_classify_seeded.restype = ctypes.c_int
-    lib.seg_debug_classify_seeded.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    lib.seg_debug_classify_seeded.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp]
     lib.seg_profile_enable.restype = ctypes.c_int
     lib.seg_profile_enable.argtypes = [vp, i32]
     lib.seg_profile_read.restype = ctypes.c_int
@@ -119,8 +119,10 @@ def seg_plan_tiles(centroids, bundle_id, M: int, B: int, max_tiles: int, tile_bu
     return nt.value
 
 
-def seg_debug_classify_seeded(atlas: int, fibers, N: int, seed_keys, label, dist, stream: int | None = None) -> None:
-    _check(LIB.seg_debug_classify_seeded(atlas, _ptr(fibers), int(N), _ptr(seed_keys), _ptr(label), _ptr(dist), stream))
+def seg_debug_classify_seeded(atlas: int, fibers, N: int, seed_keys, label, dist, stats=None,
+                              stream: int | None = None) -> None:
+    _check(LIB.seg_debug_classify_seeded(atlas, _ptr(fibers), int(N), _ptr(seed_keys), _ptr(label), _ptr(dist),
+                                         _ptr(stats), stream))
 
 
 def seg_profile_enable(atlas: int, capacity: int) -> None:

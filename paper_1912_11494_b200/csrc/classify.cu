@@ -64,6 +64,48 @@ __device__ __forceinline__ float d2(float px, float py, float pz, float4 q) {
     return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
 }
 
+// Two squared distances at once with packed f32x2 arithmetic (FADD2/FMUL2/FFMA2 on sm_100a): the
+// scalar point p against the two points whose coordinates are packed in (qx, qy, qz).  Per lane it
+// is the very same sequence of round-to-nearest operations as d2(), so the values are bit-identical.
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(u64 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ float2 d2_pair(float px, float py, float pz, u64 qx, u64 qy, u64 qz) {
+    u64 dx, dy, dz, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(pk2(px, px)), "l"(qx));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(pk2(py, py)), "l"(qy));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(pk2(pz, pz)), "l"(qz));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(dx));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(dy), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(dz), "l"(r));
+    return upk2(r);
+}
+
+// The same, for the two points packed in (px, py, pz) against the scalar point q.
+__device__ __forceinline__ float2 d2_pair_b(u64 px, u64 py, u64 pz, float qx, float qy, float qz) {
+    u64 dx, dy, dz, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(px), "l"(pk2(qx, qx)));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(py), "l"(pk2(qy, qy)));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(pz), "l"(pk2(qz, qz)));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(dx));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(dy), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(dz), "l"(r));
+    return upk2(r);
+}
+__device__ __forceinline__ u64 f2u(float2 v) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+    return r;
+}
+
 // ----------------------------------------------------------------------------------------
 // a9: spatial-order prepass (counting sort on a 2^18-bucket Morton grid of point 10)
 // ----------------------------------------------------------------------------------------
@@ -147,30 +189,34 @@ cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
 // ----------------------------------------------------------------------------------------
 // a1-a8: the classify kernel
 //
-// CTA = NCW consumer warps (one fiber per lane) + 1 producer warp that streams the CTA's listed
-// atlas tiles (64-B header + [21][32] float4 points) through a STAGES-deep shared-memory ring
-// with 1-D TMA bulk copies (cp.async.bulk -> UBLKCP), completion on mbarriers.
-// Per listed tile and consumer warp:
-//   a2  exact sphere lower bound per lane (points 0/10/20 vs the tile's spheres), warp ballot;
-//   a3  test1, dense and transposed: lane c holds centroid c's point 10 and the warp walks its
-//       passing fibers; one ballot per fiber gives that fiber's survivors against its cutoff
-//       tau = min(thr_b^2, best^2), pushed straight into a small queue q1;
-//   a4  test2, compacted: q1 is processed 32 entries at a time with every lane busy: end points
-//       in both orientations; each orientation still under tau goes to queue q2 with its max;
-//   a5/a6 test3 + test4, compacted: q2 entries are processed 32 at a time: points {3,17,7,13},
-//       then the rest with an early exit after every group;
+// CTA = NCW consumer warps (one fiber per consumer lane) + 1 producer warp.
+//   a1  fiber ingest, coalesced: each warp loads its 32 fibers (any order, through the prepass
+//       permutation) with 2 coalesced loads per fiber into shared memory: end points packed for
+//       FFMA2, point 10, and the other 18 points in xy/z planes.
+//   a2  the PRODUCER warp culls: for every bundle and then every tile of a surviving bundle it
+//       tests all FPC fibers of the CTA (4 per lane) against the exact sphere lower bounds with the
+//       fibers' live cutoffs tau = min(thr_b^2, best^2) (read from shared memory, so the cull
+//       tightens as the consumers find matches); a tile some fiber may need is copied into a
+//       STAGES-deep ring by a 1-D TMA bulk copy (cp.async.bulk -> UBLKCP, mbarrier completion),
+//       together with one lane mask per consumer warp.  An end marker closes the stream.
+//   a3+a4  consumers, dense and transposed: lane c holds centroid c's points 0/10/20 (end points
+//       packed), the warp walks the fibers of its mask: test1 (centre point) and test2 (end points,
+//       both orientations, FFMA2) for all 32 centroids at once;
+//   a5+a6  survivors go best-first to candidate rounds (32 candidates per round, every lane busy):
+//       per fiber the centroid with the smallest 3-point score first, then the rest, each re-checked
+//       against the freshest best; test3 = points {3,17,7,13}, test4 = the rest with an early exit
+//       after every group;
 //   a7  a finished orientation updates its fiber's best (d^2, bundle) key with a shared-memory
-//       64-bit atomicMin (lexicographic, so tile order and orientation never matter).
-// Fiber coordinates live in shared memory (per warp: xy plane float2 [21][32] + z plane float
-// [21][32]) so any lane can process any lane's candidate; points 0/10/20 also stay in registers.
+//       64-bit atomicMin (lexicographic, so tile order and orientation never matter);
+//   a8  epilogue: label / sqrt(d^2) stored through the permutation.
 // ----------------------------------------------------------------------------------------
-constexpr int NCW = 4;                 // consumer warps
+constexpr int NCW = 8;                 // consumer warps
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
 constexpr int STAGES = 3;              // tile ring depth
-constexpr int FB = 4;                  // fibers per step of the transposed test1 loop
-constexpr int Q1CAP = 32 + FB * 32;    // < 32 carried + up to 32 pushed per fiber of a step
-constexpr int Q2CAP = 96;              // < 32 carried + up to 64 pushed per q1 round
+constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop
+constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
+constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
 
@@ -179,23 +225,33 @@ enum {
     ST_PDIST, ST_SPHERE, ST_CTAS, ST_N
 };
 
+struct StageMeta {
+    int tile;              // tile index, -1 = end of stream
+};
+
 struct SmemLayout {
-    size_t ring, fxy, fz, q1, q2e, q2r, best, bars, tbits, bbits, total;
-    __host__ __device__ SmemLayout(int B, int T) {
+    size_t ring, fxy, fz, fe, fez, fm, pe, pr, q2e, q2r, best, bars, meta, total;
+    __host__ __device__ SmemLayout() {
         size_t o = 0;
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
-        fxy = o;  o += (size_t)NCW * NPTS * 32 * sizeof(float2);
-        fz = o;   o += (size_t)NCW * NPTS * 32 * sizeof(float);
-        best = o; o += (size_t)NCW * 32 * sizeof(unsigned long long);
+        fxy = o;  o += (size_t)NCW * NMID * 32 * sizeof(float2);
+        fz = o;   o += (size_t)NCW * NMID * 32 * sizeof(float);
+        fe = o;   o += (size_t)FPC * sizeof(float4);   // (x0, x20, y0, y20)
+        fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = 1 if the fiber is finite
+        fez = o;  o += (size_t)FPC * sizeof(float2);   // (z0, z20)
+        best = o; o += (size_t)FPC * sizeof(unsigned long long);
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
+        pe = o;   o += (size_t)NCW * 32 * sizeof(uint32_t);
+        pr = o;   o += (size_t)NCW * 32 * sizeof(float);
         q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint32_t);
         q2r = o;  o += (size_t)NCW * Q2CAP * sizeof(float);
-        q1 = o;   o += (size_t)NCW * Q1CAP * sizeof(uint16_t);
-        tbits = o; o += sizeof(uint32_t) * (size_t)((T + 31) >> 5);
-        bbits = o; o += sizeof(uint32_t) * (size_t)((B + 31) >> 5);
+        meta = o; o += (size_t)STAGES * sizeof(StageMeta);
         total = (o + 127) & ~(size_t)127;
     }
 };
+
+// plane slot of fiber point i (i != 0, 10, 20)
+__host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
 
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
@@ -212,39 +268,43 @@ __device__ __forceinline__ float key_d2(unsigned long long k) { return __uint_as
 // a2: exact tile lower bound: for every centroid c of the tile,
 // d_ME >= |f10 - c10| >= |f10 - C10| - R10 and d_ME >= min over orientations of the end-point
 // maximum, each term bounded the same way.  Skip iff the bound exceeds s = sqrt(tau) + CULL_EPS.
-__device__ __forceinline__ bool tile_may_pass(const float3 &f0, const float3 &f10, const float3 &f20,
+__device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez, const float4 &F10,
                                               const TileHdr &h, float s) {
     const float r0 = h.s0.w + s, r10 = h.s10.w + s, r20 = h.s20.w + s;
     const float a0 = r0 * r0, a10 = r10 * r10, a20 = r20 * r20;
-    const bool p10 = d2(f10.x, f10.y, f10.z, h.s10) <= a10;
-    const bool pdir = d2(f0.x, f0.y, f0.z, h.s0) <= a0 && d2(f20.x, f20.y, f20.z, h.s20) <= a20;
-    const bool pinv = d2(f0.x, f0.y, f0.z, h.s20) <= a20 && d2(f20.x, f20.y, f20.z, h.s0) <= a0;
+    const bool p10 = d2(F10.x, F10.y, F10.z, h.s10) <= a10;
+    const bool pdir = d2(E.x, E.z, Ez.x, h.s0) <= a0 && d2(E.y, E.w, Ez.y, h.s20) <= a20;
+    const bool pinv = d2(E.x, E.z, Ez.x, h.s20) <= a20 && d2(E.y, E.w, Ez.y, h.s0) <= a0;
     return p10 && (pdir || pinv);
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(NTHREADS, 3) k_classify(ClassifyParams p) {
+__global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLayout L(p.B, p.T);
+    const SmemLayout L;
     float4 *ring = reinterpret_cast<float4 *>(smem + L.ring);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
     uint64_t *empty = full + STAGES;
-    uint32_t *tbits = reinterpret_cast<uint32_t *>(smem + L.tbits);
-    uint32_t *bbits = reinterpret_cast<uint32_t *>(smem + L.bbits);
-    const int twords = (p.T + 31) >> 5;
-    const int bwords = (p.B + 31) >> 5;
+    StageMeta *meta = reinterpret_cast<StageMeta *>(smem + L.meta);
+    float4 *fe_all = reinterpret_cast<float4 *>(smem + L.fe);
+    float4 *fm_all = reinterpret_cast<float4 *>(smem + L.fm);
+    float2 *fez_all = reinterpret_cast<float2 *>(smem + L.fez);
+    unsigned long long *best_all = reinterpret_cast<unsigned long long *>(smem + L.best);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool consumer = warp < NCW;
     const int cw = consumer ? warp : 0;
-    float2 *fxy = reinterpret_cast<float2 *>(smem + L.fxy) + cw * (NPTS * 32);   // [21][32]
-    float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NPTS * 32);       // [21][32]
-    unsigned long long *best = reinterpret_cast<unsigned long long *>(smem + L.best) + cw * 32;
-    uint16_t *q1 = reinterpret_cast<uint16_t *>(smem + L.q1) + cw * Q1CAP;
+    float2 *fxy = reinterpret_cast<float2 *>(smem + L.fxy) + cw * (NMID * 32);   // [18][32]
+    float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NMID * 32);       // [18][32]
+    float4 *fe = fe_all + cw * 32;
+    float4 *fm = fm_all + cw * 32;
+    float2 *fez = fez_all + cw * 32;
+    unsigned long long *best = best_all + cw * 32;
+    uint32_t *pe = reinterpret_cast<uint32_t *>(smem + L.pe) + cw * 32;
+    float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * 32;
     uint32_t *q2e = reinterpret_cast<uint32_t *>(smem + L.q2e) + cw * Q2CAP;
     float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2CAP;
 
-    for (int i = threadIdx.x; i < twords + bwords; i += NTHREADS) tbits[i] = 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, 1);
@@ -252,236 +312,189 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_classify(ClassifyParams p) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-
-    // ---- a1: fiber ingest: 63 floats -> smem planes; points 0/10/20 kept in registers ----
-    const int gi = blockIdx.x * FPC + warp * 32 + lane;
-    const bool inrange = consumer && gi < p.n;
-    const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : 0;
-    bool finite = inrange;
-    float3 f0 = make_float3(0.f, 0.f, 0.f), f10 = f0, f20 = f0;
-    if (consumer) {
-        const float *src = p.fibers + (size_t)fidx * (3 * NPTS);
-#pragma unroll
-        for (int i = 0; i < NPTS; ++i) {
-            float x = 0.f, y = 0.f, z = 0.f;
-            if (inrange) {
-                x = __ldg(src + 3 * i);
-                y = __ldg(src + 3 * i + 1);
-                z = __ldg(src + 3 * i + 2);
-            }
-            finite = finite && isfinite(x) && isfinite(y) && isfinite(z);
-            fxy[i * 32 + lane] = make_float2(x, y);
-            fz[i * 32 + lane] = z;
-            if (i == 0) f0 = make_float3(x, y, z);
-            if (i == 10) f10 = make_float3(x, y, z);
-            if (i == 20) f20 = make_float3(x, y, z);
-        }
-        best[lane] = (p.seed && inrange) ? p.seed[fidx] : KEY_NONE;
-    }
     unsigned long long cnt[ST_N];
     if (STATS) {
 #pragma unroll
         for (int k = 0; k < ST_N; ++k) cnt[k] = 0;
-        cnt[ST_FIBERS] = inrange ? 1 : 0;
         cnt[ST_CTAS] = threadIdx.x == 0 ? 1 : 0;
     }
-    __syncthreads();
 
-    // ---- a2 (pre-pass): CTA candidate list from the threshold-only bound ----
+    // ---- a1: coalesced fiber ingest (consumer warps) ----
+    const int gi = blockIdx.x * FPC + warp * 32 + lane;
+    const bool inrange = consumer && gi < p.n;
+    const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
     if (consumer) {
-        for (int b0 = 0; b0 < p.B; b0 += 32) {
-            uint32_t m = 0;
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-                const int b = b0 + j;
-                if (b < p.B) {
-                    const BundleHdr h = p.bh[b];
-                    const float r = h.s10.w + h.thr + CULL_EPS;
-                    const bool pass = h.t1 > h.t0 && finite && d2(f10.x, f10.y, f10.z, h.s10) <= r * r;
-                    m |= (pass ? 1u : 0u) << j;
+        // this lane loads floats k0 = lane and k1 = 32 + lane (k1 < 63) of every fiber of the warp,
+        // 8 fibers per batch so 16 loads per lane are in flight before the first store
+        const int k0 = lane, k1 = 32 + lane;
+        const int p0 = k0 / 3, c0 = k0 % 3, p1 = k1 / 3, c1 = k1 % 3;
+        auto put = [&](int j, int pt, int c, float v) {
+            // fe = (x0, x20, y0, y20), fez = (z0, z20), fm = (x10, y10, z10, finite)
+            if (pt == 0 || pt == 20) {
+                if (c < 2) reinterpret_cast<float *>(fe + j)[2 * c + (pt == 20 ? 1 : 0)] = v;
+                else reinterpret_cast<float *>(fez + j)[pt == 20 ? 1 : 0] = v;
+            } else if (pt == 10) {
+                reinterpret_cast<float *>(fm + j)[c] = v;
+            } else if (c < 2) {
+                reinterpret_cast<float *>(fxy + mid_slot(pt) * 32 + j)[c] = v;
+            } else {
+                fz[mid_slot(pt) * 32 + j] = v;
+            }
+        };
+        uint32_t fin = 0;   // bit j: this lane's two values of fiber j are finite
+        for (int jb = 0; jb < 32; jb += 8) {
+            float v0[8], v1[8];
+            int fjs[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int fj = __shfl_sync(0xffffffffu, fidx, jb + q);
+                fjs[q] = fj;
+                v0[q] = 0.f;
+                v1[q] = 0.f;
+                if (fj >= 0) {
+                    const float *src = p.fibers + (size_t)fj * (3 * NPTS);
+                    v0[q] = __ldg(src + k0);
+                    if (k1 < 3 * NPTS) v1[q] = __ldg(src + k1);
                 }
             }
-            if (STATS && finite) { cnt[ST_SPHERE] += min(32, p.B - b0); cnt[ST_PDIST] += min(32, p.B - b0); }
-            m = __reduce_or_sync(0xffffffffu, m);
-            if (lane == 0 && m) atomicOr(bbits + (b0 >> 5), m);
-        }
-    }
-    __syncthreads();
-    if (consumer) {
-        for (int w = 0; w < bwords; ++w) {
-            uint32_t bits = bbits[w];
-            while (bits) {
-                const int b = (w << 5) + __ffs(bits) - 1;
-                bits &= bits - 1;
-                const BundleHdr h = p.bh[b];
-                const float s = h.thr + CULL_EPS;
-                const float r = h.s10.w + s;
-                const bool bpass = finite && d2(f10.x, f10.y, f10.z, h.s10) <= r * r;
-                if (!__any_sync(0xffffffffu, bpass)) continue;
-                for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
-                    uint32_t m = 0;
-                    const int nt = min(32, h.t1 - t0);
-#pragma unroll 4
-                    for (int j = 0; j < 32; ++j) {
-                        if (j < nt) {
-                            const TileHdr th = p.th[t0 + j];
-                            m |= (bpass && tile_may_pass(f0, f10, f20, th, s) ? 1u : 0u) << j;
-                        }
-                    }
-                    if (STATS && bpass) { cnt[ST_SPHERE] += nt; cnt[ST_PDIST] += 5 * nt; }
-                    m = __reduce_or_sync(0xffffffffu, m);
-                    if (lane == 0 && m) {
-                        // tiles t0..t0+nt-1 -> bit positions; may straddle two words
-                        const int w0 = t0 >> 5, sh = t0 & 31;
-                        atomicOr(tbits + w0, m << sh);
-                        if (sh && (m >> (32 - sh))) atomicOr(tbits + w0 + 1, m >> (32 - sh));
-                    }
-                }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int j = jb + q;
+                if (isfinite(v0[q]) && isfinite(v1[q]) && fjs[q] >= 0) fin |= 1u << j;
+                put(j, p0, c0, v0[q]);
+                if (k1 < 3 * NPTS) put(j, p1, c1, v1[q]);
             }
         }
+        fin = __reduce_and_sync(0xffffffffu, fin);   // bit j: every value of fiber j is finite
+        fm[lane].w = ((fin >> lane) & 1u) ? 1.f : 0.f;
+        best[lane] = (p.seed && inrange) ? p.seed[fidx] : KEY_NONE;
+        if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
     __syncthreads();
 
     if (!consumer) {
-        // ---- producer warp: TMA bulk copies of the listed tiles into the ring ----
+        // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
         if (lane == 0) {
+            const uint32_t *bits_g = p.tile_bits + (size_t)blockIdx.x * ((p.T + 31) >> 5);
             int k = 0;
-            for (int w = 0; w < twords; ++w) {
-                uint32_t bits = tbits[w];
+            for (int w = 0; w < ((p.T + 31) >> 5); ++w) {
+                uint32_t bits = __ldg(bits_g + w);
                 while (bits) {
                     const int t = (w << 5) + __ffs(bits) - 1;
                     bits &= bits - 1;
                     const int s = k % STAGES, u = k / STAGES;
                     if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
+                    meta[s].tile = t;
                     mbar_arrive_expect_tx(full + s, TILE_STRIDE_BYTES);
                     bulk_g2s(ring + s * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES,
                              full + s);
                     ++k;
                 }
             }
+            const int s = k % STAGES, u = k / STAGES;   // end of stream
+            if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
+            meta[s].tile = -1;
+            mbar_arrive(full + s);
         }
-        return;
-    }
-
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    int k = 0;
-    for (int w = 0; w < twords; ++w) {
-        uint32_t bits = tbits[w];
-        while (bits) {
-            bits &= bits - 1;
+    } else {
+        // ---- consumers ----
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        const float4 myE = fe[lane], myF10 = fm[lane];
+        const float2 myEz = fez[lane];
+        const bool myok = myF10.w != 0.f;
+        for (int k = 0;; ++k) {
             const int s = k % STAGES, u = k / STAGES;
-            ++k;
             mbar_sleep_wait(full + s, u & 1);
+            if (meta[s].tile < 0) break;
             const float4 *stage = ring + s * TILE_STRIDE_F4;
             const TileHdr th = *reinterpret_cast<const TileHdr *>(stage);
-            const float4 *T = stage + TILE_HDR_F4;
             const float thr2 = th.thr2;
             const int b = th.bundle;
             const float tau = fminf(thr2, key_d2(best[lane]));
-            const bool pass = finite && tile_may_pass(f0, f10, f20, th, sqrtf(tau) + CULL_EPS);
+            // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
+            const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sqrtf(tau) + CULL_EPS);
+            uint32_t pm = __ballot_sync(0xffffffffu, pass);
+#if defined(SEG_EXP) && SEG_EXP == 1
+            pm = 0;  // experiment: tile loop overhead only
+#endif
             if (STATS) {
                 if (lane == 0) cnt[ST_WT_LISTED]++;
-                if (finite) { cnt[ST_SPHERE]++; cnt[ST_PDIST] += 5; }
+                if (myok) { cnt[ST_SPHERE]++; cnt[ST_PDIST] += 5; }
             }
-            if (__any_sync(0xffffffffu, pass)) {
+            if (pm) {
+                const float4 *T = stage + TILE_HDR_F4;
                 if (STATS) {
                     if (lane == 0) cnt[ST_WT_COMPUTED]++;
-                    if (pass) { cnt[ST_LT_PASS]++; cnt[ST_T1] += TILE; cnt[ST_PDIST] += TILE; }
+                    if ((pm >> lane) & 1u) { cnt[ST_LT_PASS]++; cnt[ST_T1] += TILE; cnt[ST_PDIST] += TILE; }
                 }
-                // ---- q2 round: test3 + test4 on entries [base, base + cnt2) ----
-                auto run_q2 = [&](int base, int cnt2) {
-                    if (lane < cnt2) {
-                        const uint32_t e = q2e[base + lane];
-                        float r = q2r[base + lane];
+                // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
+                // starting from its 3-point running max r
+                auto run_cand = [&](const uint32_t *qe, const float *qr, int n) {
+#if defined(SEG_EXP) && SEG_EXP == 2
+                    n = 0;  // experiment: no candidate rounds
+#endif
+                    if (lane < n) {
+                        const uint32_t e = qe[lane];
+                        float r = qr[lane];
                         const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1;
                         const float taul = fminf(thr2, key_d2(best[fl]));
-                        const float4 *cb = T + c + (o ? 20 * TILE : 0);
-                        const int st = o ? -TILE : TILE;
-                        bool done = false;
+                        if (r <= taul) {  // re-check against the freshest best (best-first pays here)
+                            const float4 *cb = T + c + (o ? 20 * TILE : 0);
+                            const int st = o ? -TILE : TILE;
+                            bool done = false;
 #define SEG_STEP(i)                                                             \
     {                                                                           \
-        const float2 a = fxy[(i) * 32 + fl];                                    \
-        r = fmaxf(r, d2(a.x, a.y, fz[(i) * 32 + fl], cb[(i) * st]));            \
+        const float2 a = fxy[mid_slot(i) * 32 + fl];                            \
+        r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
     }
-                        if (STATS) cnt[ST_T34]++;
-                        SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
-                        if (STATS) cnt[ST_PDIST] += 4;
-                        if (r > taul) done = true;
-                        if (!done) {
-                            SEG_STEP(10); SEG_STEP(1); SEG_STEP(19); SEG_STEP(2);
+                            if (STATS) cnt[ST_T34]++;
+                            SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
                             if (STATS) cnt[ST_PDIST] += 4;
                             if (r > taul) done = true;
-                        }
-                        if (!done) {
-                            SEG_STEP(18); SEG_STEP(4); SEG_STEP(16); SEG_STEP(5);
-                            if (STATS) cnt[ST_PDIST] += 4;
-                            if (r > taul) done = true;
-                        }
-                        if (!done) {
-                            SEG_STEP(15); SEG_STEP(6); SEG_STEP(14); SEG_STEP(8); SEG_STEP(12);
-                            SEG_STEP(9); SEG_STEP(11);
-                            if (STATS) { cnt[ST_PDIST] += 7; cnt[ST_FULL]++; }
-                            // a7: lexicographic (d^2, bundle) minimum
-                            if (r <= thr2) {
-                                atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
-                                if (STATS) cnt[ST_UPD]++;
+                            if (!done) {
+                                SEG_STEP(1); SEG_STEP(19); SEG_STEP(5); SEG_STEP(15);
+                                if (STATS) cnt[ST_PDIST] += 4;
+                                if (r > taul) done = true;
                             }
-                        }
+                            if (!done) {
+                                SEG_STEP(2); SEG_STEP(18); SEG_STEP(4); SEG_STEP(16);
+                                if (STATS) cnt[ST_PDIST] += 4;
+                                if (r > taul) done = true;
+                            }
+                            if (!done) {
+                                SEG_STEP(6); SEG_STEP(14); SEG_STEP(8); SEG_STEP(12); SEG_STEP(9);
+                                SEG_STEP(11);
+                                if (STATS) { cnt[ST_PDIST] += 6; cnt[ST_FULL]++; }
+                                // a7: lexicographic (d^2, bundle) minimum
+                                if (r <= thr2) {
+                                    atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
+                                    if (STATS) cnt[ST_UPD]++;
+                                }
+                            }
 #undef SEG_STEP
+                        }
                     }
                     __syncwarp();
                 };
-
-                // ---- q1 round: test2 on entries [base, base + cnt1), survivors pushed to q2 ----
-                int n2 = 0;
-                auto run_q1 = [&](int base, int cnt1) {
-                    bool ad = false, ai = false;
-                    uint32_t e = 0;
-                    float rd = 0.f, ri = 0.f;
-                    if (lane < cnt1) {
-                        e = q1[base + lane];
-                        const int fl = e >> 5, c = e & 31;
-                        const float taul = fminf(thr2, key_d2(best[fl]));
-                        const float2 a0 = fxy[fl], a20 = fxy[20 * 32 + fl];
-                        const float z0 = fz[fl], z20 = fz[20 * 32 + fl];
-                        const float4 c0 = T[c], c20 = T[20 * TILE + c];
-                        const float e00 = d2(a0.x, a0.y, z0, c0), e2020 = d2(a20.x, a20.y, z20, c20);
-                        const float e020 = d2(a0.x, a0.y, z0, c20), e200 = d2(a20.x, a20.y, z20, c0);
-                        rd = fmaxf(e00, e2020);
-                        ri = fmaxf(e020, e200);
-                        ad = rd <= taul;
-                        ai = ri <= taul;
-                        if (STATS) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
-                    }
-                    const uint32_t bd = __ballot_sync(0xffffffffu, ad), bi = __ballot_sync(0xffffffffu, ai);
-                    if (ad) {
-                        const int pos = n2 + __popc(bd & lt_mask);
-                        q2e[pos] = e;
-                        q2r[pos] = rd;
-                    }
-                    if (ai) {
-                        const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
-                        q2e[pos] = e | (1u << 10);
-                        q2r[pos] = ri;
-                    }
-                    n2 += __popc(bd) + __popc(bi);
+                int np = 0, n2 = 0;
+                auto flush = [&](int keep) {   // best-first: the per-fiber winners, then the rest
                     __syncwarp();
-                    while (n2 >= 32) {
-                        n2 -= 32;
-                        run_q2(n2, 32);
+                    if (np) run_cand(pe, pr, np);
+                    np = 0;
+                    while (n2 > keep) {
+                        const int m = n2 >= 32 ? 32 : n2;
+                        n2 -= m;
+                        run_cand(q2e + n2, q2r + n2, m);
                     }
                 };
-
-                // ---- a3, test1 (dense, transposed): lane c holds centroid c's point 10; the warp
-                // walks its passing fibers j (broadcast point 10 from smem) and one ballot per
-                // fiber yields that fiber's survivor set, pushed straight into q1 ----
-                const float4 cc10 = T[10 * TILE + lane];
-                uint32_t pm = __ballot_sync(0xffffffffu, pass);
-                int n1 = 0;
+                // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
+                const float4 c10 = T[10 * TILE + lane];
+                const float4 c0 = T[lane], c20 = T[20 * TILE + lane];
                 while (pm) {
-                    // up to FB fibers per step: independent distance chains for ILP
+                    // FB fibers per step: independent chains (ILP) and one warp vote per step
                     int jj[FB];
-                    bool ok[FB];
+                    float rdv[FB], riv[FB], tjv[FB];
+                    uint32_t hit = 0;
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         jj[q] = pm ? __ffs(pm) - 1 : -1;
@@ -490,48 +503,83 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_classify(ClassifyParams p) {
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         const int j = jj[q] < 0 ? 0 : jj[q];
-                        const float2 a = fxy[10 * 32 + j];
-                        const float m10 = d2(a.x, a.y, fz[10 * 32 + j], cc10);
-                        ok[q] = jj[q] >= 0 && m10 <= __shfl_sync(0xffffffffu, tau, j);
+                        // fiber j's end points arrive packed: (x0, x20), (y0, y20), (z0, z20)
+                        const float4 E = fe[j];
+                        const float2 Ez = fez[j];
+                        const float4 a10 = fm[j];
+                        const float tj = __shfl_sync(0xffffffffu, tau, j);
+                        const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)), EZ = f2u(Ez);
+                        const float m10 = d2(a10.x, a10.y, a10.z, c10);                 // test1
+                        const float2 R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);      // (e0,0, e20,0)
+                        const float2 R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);  // (e0,20, e20,20)
+                        rdv[q] = fmaxf(fmaxf(m10, R0.x), R20.y);                        // test2, direct
+                        riv[q] = fmaxf(fmaxf(m10, R20.x), R0.y);                        // test2, inverse
+                        tjv[q] = tj;
+                        if (jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj) hit |= 1u << q;
+                        if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
+                    hit = __reduce_or_sync(0xffffffffu, hit);
+                    if (!hit) continue;
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
-                        const uint32_t bal = __ballot_sync(0xffffffffu, ok[q]);
-                        if (ok[q]) q1[n1 + __popc(bal & lt_mask)] = (uint16_t)((jj[q] << 5) | lane);
-                        n1 += __popc(bal);
-                    }
-                    __syncwarp();
-                    while (n1 >= 32) {
-                        n1 -= 32;
-                        run_q1(n1, 32);
+                        if (!((hit >> q) & 1u)) continue;
+                        const int j = jj[q];
+                        const float rd = rdv[q], ri = riv[q], tj = tjv[q];
+                        const bool ad = rd <= tj, ai = ri <= tj;
+                        // best-first: the centroid with the smallest 3-point score goes to the
+                        // winners' round, every other surviving orientation to q2
+                        const float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
+                        const uint32_t sb = __float_as_uint(sc);
+                        const uint32_t smin = __reduce_min_sync(0xffffffffu, sb);
+                        const int wl = __ffs(__ballot_sync(0xffffffffu, sb == smin)) - 1;
+                        const bool win = lane == wl;
+                        const int wo = (ad && rd == sc) ? 0 : 1;
+                        const uint32_t e = (uint32_t)((j << 5) | lane);
+                        if (win) {
+                            pe[np] = e | ((uint32_t)wo << 10);
+                            pr[np] = sc;
+                        }
+                        ++np;
+                        const bool qd = ad && !(win && wo == 0), qi = ai && !(win && wo == 1);
+                        const uint32_t bd = __ballot_sync(0xffffffffu, qd), bi = __ballot_sync(0xffffffffu, qi);
+                        if (qd) {
+                            const int pos = n2 + __popc(bd & lt_mask);
+                            q2e[pos] = e;
+                            q2r[pos] = rd;
+                        }
+                        if (qi) {
+                            const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
+                            q2e[pos] = e | (1u << 10);
+                            q2r[pos] = ri;
+                        }
+                        n2 += __popc(bd) + __popc(bi);
+                        if (n2 > Q2CAP - 64) flush(31);
                     }
                 }
-                __syncwarp();
-                if (n1 > 0) run_q1(0, n1);
-                if (n2 > 0) run_q2(0, n2);
+                flush(0);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
-    }
 
-    // ---- a8: epilogue ----
-    if (inrange) {
-        const unsigned long long key = best[lane];
-        int lab;
-        float dd;
-        if (!finite) {
-            lab = -1;
-            dd = __int_as_float(0x7fffffff);  // NaN
-        } else if (key != KEY_NONE) {
-            lab = (int)(uint32_t)(key & 0xffffffffu);
-            dd = __fsqrt_rn(key_d2(key));
-        } else {
-            lab = -1;
-            dd = INFINITY;
+        // ---- a8: epilogue ----
+        if (inrange) {
+            const unsigned long long key = best[lane];
+            int lab;
+            float dd;
+            if (fm[lane].w == 0.f) {
+                lab = -1;
+                dd = __int_as_float(0x7fffffff);  // NaN: non-finite fiber
+            } else if (key != KEY_NONE) {
+                lab = (int)(uint32_t)(key & 0xffffffffu);
+                dd = __fsqrt_rn(key_d2(key));
+            } else {
+                lab = -1;
+                dd = INFINITY;
+            }
+            p.label[fidx] = lab;
+            p.dist[fidx] = dd;
         }
-        p.label[fidx] = lab;
-        p.dist[fidx] = dd;
     }
     if (STATS) {
 #pragma unroll
@@ -544,15 +592,96 @@ __global__ void __launch_bounds__(NTHREADS, 3) k_classify(ClassifyParams p) {
     }
 }
 
-size_t classify_smem_bytes(int B, int T) { return SmemLayout(B, T).total; }
+// ----------------------------------------------------------------------------------------
+// a2 (list): k_cull -- per CTA of the classify kernel (the same FPC fibers), the set of tiles some
+// fiber may need under its bundle threshold: bundle test on the point-10 sphere, then the 3-sphere
+// tile test for the tiles of the surviving bundles.  Written as one bitset per CTA.  A separate,
+// light kernel (no big shared-memory ring) so its latency-bound header loads run at full occupancy.
+// ----------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
+    extern __shared__ uint32_t sbits[];          // [twords] tile bits, then [bwords] bundle bits
+    const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
+    uint32_t *tb = sbits, *bb = sbits + twords;
+    for (int i = threadIdx.x; i < twords + bwords; i += FPC) sbits[i] = 0;
+    const int lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * FPC + threadIdx.x;
+    bool ok = gi < p.n;
+    float4 E = make_float4(0.f, 0.f, 0.f, 0.f), F10 = E;
+    float2 Ez = make_float2(0.f, 0.f);
+    if (ok) {
+        const int fidx = p.perm ? __ldg(p.perm + gi) : gi;
+        const float *src = p.fibers + (size_t)fidx * (3 * NPTS);
+        E = make_float4(__ldg(src + 0), __ldg(src + 60), __ldg(src + 1), __ldg(src + 61));
+        Ez = make_float2(__ldg(src + 2), __ldg(src + 62));
+        F10 = make_float4(__ldg(src + 30), __ldg(src + 31), __ldg(src + 32), 0.f);
+        ok = isfinite(E.x) && isfinite(E.y) && isfinite(E.z) && isfinite(E.w) && isfinite(Ez.x) && isfinite(Ez.y) &&
+             isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
+    }
+    __syncthreads();
+    for (int b0 = 0; b0 < p.B; b0 += 32) {
+        uint32_t m = 0;
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const int b = b0 + j;
+            if (b < p.B) {
+                const BundleHdr h = p.bh[b];
+                const float r = h.s10.w + h.thr + CULL_EPS;
+                const bool pass = ok && h.t1 > h.t0 && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
+                m |= (pass ? 1u : 0u) << j;
+            }
+        }
+        m = __reduce_or_sync(0xffffffffu, m);
+        if (lane == 0 && m) atomicOr(bb + (b0 >> 5), m);
+    }
+    __syncthreads();
+    for (int w = 0; w < bwords; ++w) {
+        uint32_t bits = bb[w];
+        while (bits) {
+            const int b = (w << 5) + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const BundleHdr h = p.bh[b];
+            const float sv = h.thr + CULL_EPS;
+            const float r = h.s10.w + sv;
+            const bool bpass = ok && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
+            if (!__any_sync(0xffffffffu, bpass)) continue;
+            for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
+                uint32_t m = 0;
+                const int nt = min(32, h.t1 - t0);
+#pragma unroll 4
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nt) {
+                        const TileHdr th = p.th[t0 + j];
+                        m |= (bpass && tile_may_pass(E, Ez, F10, th, sv) ? 1u : 0u) << j;
+                    }
+                }
+                m = __reduce_or_sync(0xffffffffu, m);
+                if (lane == 0 && m) {
+                    const int w0 = t0 >> 5, sh = t0 & 31;
+                    atomicOr(tb + w0, m << sh);
+                    if (sh && (m >> (32 - sh))) atomicOr(tb + w0 + 1, m >> (32 - sh));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t *out = p.tile_bits + (size_t)blockIdx.x * twords;
+    for (int i = threadIdx.x; i < twords; i += FPC) out[i] = tb[i];
+}
+
+size_t classify_smem_bytes(int, int) { return SmemLayout().total; }
 
 int classify_fibers_per_cta() { return FPC; }
+
+size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)((T + 31) >> 5); }
 
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s) {
     if (p.n <= 0) return cudaSuccess;
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
-    cudaError_t e;
+    const size_t cull_smem = sizeof(uint32_t) * (size_t)(((p.T + 31) >> 5) + ((p.B + 31) >> 5));
+    cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
+    if (e != cudaSuccess) return e;
+    k_cull<<<grid, FPC, cull_smem, s>>>(p);
     if (stats) {
         e = cudaFuncSetAttribute(k_classify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

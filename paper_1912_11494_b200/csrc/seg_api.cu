@@ -460,10 +460,14 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
         MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, perm};
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
-    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats};
+    uint32_t *tbits = nullptr;
+    SEG_CUDA(cudaMallocAsync((void **)&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T), s),
+             "seg_classify: cudaMallocAsync");
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
+    cudaFreeAsync(tbits, s);
     if (key) {
         cudaFreeAsync(key, s);
         cudaFreeAsync(perm, s);
@@ -646,7 +650,7 @@ extern "C" int seg_profile_read(seg_atlas *a, float *prepass_ms, float *classify
 }
 
 extern "C" int seg_debug_classify_seeded(const seg_atlas *a, const float *fibers, int64_t N, const uint64_t *seed,
-                                         int32_t *label, float *dist, void *stream) {
+                                         int32_t *label, float *dist, uint64_t *stats, void *stream) {
     if (!seed && N > 0) return fail(SEG_EINVAL, "seg_debug_classify_seeded: null seed_keys");
-    return classify_common(a, fibers, N, label, dist, stream, nullptr, seed);
+    return classify_common(a, fibers, N, label, dist, stream, stats, seed);
 }

@@ -48,6 +48,7 @@ struct ClassifyParams {
     const BundleHdr *bh;      // [B]
     int B, T;
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
+    uint32_t *tile_bits;       // [ceil(n / FPC)][ceil(T / 32)] scratch: k_cull -> k_classify
 };
 
 struct MortonParams {
@@ -64,6 +65,7 @@ struct MortonParams {
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s);
 size_t classify_smem_bytes(int B, int T);
+size_t cull_bits_words(int n, int T);
 int classify_fibers_per_cta();
 
 }  // namespace seg

@@ -38,8 +38,11 @@ key = (d2.view(torch.int32).to(torch.int64) << 32) | lab0.to(torch.int64).bitwis
 key = torch.where(lab0 >= 0, key, torch.full_like(key, -1))
 lab2 = torch.empty_like(lab)
 d2o = torch.empty_like(d)
-t1 = timeit(lambda: binding.seg_debug_classify_seeded(A.handle, fib, N, key, lab2, d2o,
+t1 = timeit(lambda: binding.seg_debug_classify_seeded(A.handle, fib, N, key, lab2, d2o, None,
                                                       torch.cuda.current_stream().cuda_stream))
+st2 = np.zeros(binding.SEG_NSTATS, np.uint64)
+binding.seg_debug_classify_seeded(A.handle, fib, N, key, lab2, d2o, st2, torch.cuda.current_stream().cuda_stream)
 same = bool(torch.equal(lab0, lab2)) and bool(torch.equal(d0.view(torch.int32), d2o.view(torch.int32)))
 print(f"cfg{cfg}: normal {t0:.3f} ms, seeded {t1:.3f} ms, identical={same}")
-print("stats", st)
+print("stats normal", st)
+print("stats seeded", dict(zip(binding.STAT_NAMES, (int(v) for v in st2))))

@@ -203,7 +203,7 @@ def test_stats_kernel_matches_and_counts():
     assert st["fibers"] == 50_000
     assert st["lane_test1"] >= st["lane_test2"] >= st["lane_test34"] >= st["lane_full21"]
     assert st["best_updates"] >= int((lab >= 0).sum())
-    assert st["ctas"] == -(-50_000 // 128)
+    assert st["ctas"] == -(-50_000 // 256)
 
 
 def test_argument_errors_on_gpu(cfg0):
