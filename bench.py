@@ -248,16 +248,19 @@ def main():
     w_instr = FP32_INSTR_PER_PDIST * st["lane_point_dists"]          # algorithmic FP32 lane-instr
     achieved = w_instr / (cls_ms * 1e-3) / 1e12                      # T lane-instr / s
     peak = sm_count * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"cfg{cfg}")
+            rec = json.load(open(tf)).get(f"cfg{cfg}")
+            traffic, traffic_src = rec["bytes"], rec["source"]
         except Exception:
             traffic = None
     roofline = dict(bound="alu", achieved=achieved, peak=peak, unit="Tinstr/s (FP32 lane-instr)",
-                    frac=achieved / peak, traffic=traffic,
-                    kernel="k_classify", kernel_ms=cls_ms, prepass_ms=pre_ms,
+                    frac=achieved / peak, traffic=traffic, traffic_unit="DRAM bytes per k_classify launch",
+                    traffic_source=traffic_src,
+                    kernel="k_cull + k_classify (timed together by the library's profile events)",
+                    kernel_ms=cls_ms, prepass_ms=pre_ms,
                     peak_basis=f"{sm_count} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_mhz:.0f} MHz "
                                f"(median SM clock during the timed region)",
                     work_basis=f"{FP32_INSTR_PER_PDIST} FP32 instr x {st['lane_point_dists']:,} lane point-distance "
