@@ -67,7 +67,8 @@ typedef struct seg_atlas seg_atlas;
  * The library copies everything; the caller may free its inputs on return.
  * Synchronous.  Bundles with no centroid are allowed (they never win).
  * Errors: SEG_EINVAL (null pointer, M < 1, B < 1, bundle id out of range, threshold
- * not finite or <= 0, non-finite centroid coordinate), SEG_ENOMEM, SEG_ECUDA.
+ * not finite or <= 0, non-finite centroid coordinate, more than 30,000 tiles -- i.e. roughly
+ * 960,000 centroids -- in this build), SEG_ENOMEM, SEG_ECUDA.
  */
 int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M,
                const float *thresh, int32_t B, int device, seg_atlas **out);

@@ -219,6 +219,8 @@ constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (sme
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
+constexpr int MAX_TILES = 30000;
+constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle headers (16 KB)       // k_cull keeps per-tile priorities and the list in shared memory
 
 enum {
     ST_FIBERS = 0, ST_WT_LISTED, ST_WT_COMPUTED, ST_LT_PASS, ST_T1, ST_T2, ST_T34, ST_FULL, ST_UPD,
@@ -276,6 +278,20 @@ __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez,
     const bool pdir = d2(E.x, E.z, Ez.x, h.s0) <= a0 && d2(E.y, E.w, Ez.y, h.s20) <= a20;
     const bool pinv = d2(E.x, E.z, Ez.x, h.s20) <= a20 && d2(E.y, E.w, Ez.y, h.s0) <= a0;
     return p10 && (pdir || pinv);
+}
+
+// tile_may_pass plus a second verdict from the same five distances: are points 0/10/20 of the fiber
+// inside the tile's spheres (in one orientation)?  k_cull orders tiles by it.
+__device__ __forceinline__ bool tile_pass_inside(const float4 &E, const float2 &Ez, const float4 &F10,
+                                                 const TileHdr &h, float s, bool &inside) {
+    const float d10 = d2(F10.x, F10.y, F10.z, h.s10);
+    const float d00 = d2(E.x, E.z, Ez.x, h.s0), d2020 = d2(E.y, E.w, Ez.y, h.s20);
+    const float d020 = d2(E.x, E.z, Ez.x, h.s20), d200 = d2(E.y, E.w, Ez.y, h.s0);
+    auto in = [](float dd, float r) { return dd <= r * r; };
+    const float r0 = h.s0.w + s, r10 = h.s10.w + s, r20 = h.s20.w + s;
+    const float q0 = h.s0.w + CULL_EPS, q10 = h.s10.w + CULL_EPS, q20 = h.s20.w + CULL_EPS;
+    inside = in(d10, q10) && ((in(d00, q0) && in(d2020, q20)) || (in(d020, q20) && in(d200, q0)));
+    return in(d10, r10) && ((in(d00, r0) && in(d2020, r20)) || (in(d020, r20) && in(d200, r0)));
 }
 
 template <bool STATS>
@@ -375,21 +391,16 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
     if (!consumer) {
         // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
         if (lane == 0) {
-            const uint32_t *bits_g = p.tile_bits + (size_t)blockIdx.x * ((p.T + 31) >> 5);
+            const int32_t *lst_g = reinterpret_cast<const int32_t *>(p.tile_bits) + (size_t)blockIdx.x * (p.T + 1);
+            const int nlist = __ldg(lst_g);
             int k = 0;
-            for (int w = 0; w < ((p.T + 31) >> 5); ++w) {
-                uint32_t bits = __ldg(bits_g + w);
-                while (bits) {
-                    const int t = (w << 5) + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const int s = k % STAGES, u = k / STAGES;
-                    if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
-                    meta[s].tile = t;
-                    mbar_arrive_expect_tx(full + s, TILE_STRIDE_BYTES);
-                    bulk_g2s(ring + s * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES,
-                             full + s);
-                    ++k;
-                }
+            for (; k < nlist; ++k) {
+                const int t = __ldg(lst_g + 1 + k);
+                const int s = k % STAGES, u = k / STAGES;
+                if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
+                meta[s].tile = t;
+                mbar_arrive_expect_tx(full + s, TILE_STRIDE_BYTES);
+                bulk_g2s(ring + s * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES, full + s);
             }
             const int s = k % STAGES, u = k / STAGES;   // end of stream
             if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
@@ -593,16 +604,27 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
 }
 
 // ----------------------------------------------------------------------------------------
-// a2 (list): k_cull -- per CTA of the classify kernel (the same FPC fibers), the set of tiles some
-// fiber may need under its bundle threshold: bundle test on the point-10 sphere, then the 3-sphere
-// tile test for the tiles of the surviving bundles.  Written as one bitset per CTA.  A separate,
-// light kernel (no big shared-memory ring) so its latency-bound header loads run at full occupancy.
+// a2 (list): k_cull -- per CTA of the classify kernel (the same FPC fibers), the tiles some fiber may
+// need under its bundle threshold: bundle test on the point-10 sphere, then the 3-sphere tile test
+// for the tiles of the surviving bundles.  Written as an ordered list per CTA ([count, tiles...]),
+// best-first (see below).  A separate, light kernel (no big shared-memory ring) so its
+// latency-bound header loads run at full occupancy.
 // ----------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
-    extern __shared__ uint32_t sbits[];          // [twords] tile bits, then [bwords] bundle bits
+    // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list, count
+    extern __shared__ uint32_t sbits[];
     const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
-    uint32_t *tb = sbits, *bb = sbits + twords;
-    for (int i = threadIdx.x; i < twords + bwords; i += FPC) sbits[i] = 0;
+    uint32_t *tb = sbits, *bb = sbits + twords, *prio = bb + bwords;
+    uint16_t *lst = reinterpret_cast<uint16_t *>(prio + p.T);
+    __shared__ int nlist;
+    __shared__ BundleHdr sbh[MAX_SMEM_BUNDLES];
+    for (int i = threadIdx.x; i < twords + bwords + p.T; i += FPC) sbits[i] = 0;
+    if (threadIdx.x == 0) nlist = 0;
+    // bundle headers staged once per CTA (broadcast reads below) when they fit
+    const bool stage_bh = p.B <= MAX_SMEM_BUNDLES;
+    if (stage_bh)
+        for (int i = threadIdx.x; i < p.B; i += FPC) sbh[i] = p.bh[i];
+    const BundleHdr *bhp = stage_bh ? sbh : p.bh;
     const int lane = threadIdx.x & 31;
     const int gi = blockIdx.x * FPC + threadIdx.x;
     bool ok = gi < p.n;
@@ -624,7 +646,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         for (int j = 0; j < 32; ++j) {
             const int b = b0 + j;
             if (b < p.B) {
-                const BundleHdr h = p.bh[b];
+                const BundleHdr h = bhp[b];
                 const float r = h.s10.w + h.thr + CULL_EPS;
                 const bool pass = ok && h.t1 > h.t0 && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
                 m |= (pass ? 1u : 0u) << j;
@@ -639,46 +661,78 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         while (bits) {
             const int b = (w << 5) + __ffs(bits) - 1;
             bits &= bits - 1;
-            const BundleHdr h = p.bh[b];
+            const BundleHdr h = bhp[b];
             const float sv = h.thr + CULL_EPS;
             const float r = h.s10.w + sv;
             const bool bpass = ok && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
             if (!__any_sync(0xffffffffu, bpass)) continue;
             for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
-                uint32_t m = 0;
+                // 32 tiles per chunk: independent header loads and tests (ILP), then bookkeeping
                 const int nt = min(32, h.t1 - t0);
+                uint32_t pm = 0, cm = 0;
 #pragma unroll 4
                 for (int j = 0; j < 32; ++j) {
                     if (j < nt) {
                         const TileHdr th = p.th[t0 + j];
-                        m |= (bpass && tile_may_pass(E, Ez, F10, th, sv) ? 1u : 0u) << j;
+                        // processing priority: fibers whose points 0/10/20 lie inside the spheres
+                        bool close;
+                        const bool pass = bpass && tile_pass_inside(E, Ez, F10, th, sv, close);
+                        close = close && pass;
+                        pm |= (pass ? 1u : 0u) << j;
+                        cm |= (close ? 1u : 0u) << j;
                     }
                 }
-                m = __reduce_or_sync(0xffffffffu, m);
-                if (lane == 0 && m) {
-                    const int w0 = t0 >> 5, sh = t0 & 31;
-                    atomicOr(tb + w0, m << sh);
-                    if (sh && (m >> (32 - sh))) atomicOr(tb + w0 + 1, m >> (32 - sh));
+                uint32_t any = __reduce_or_sync(0xffffffffu, pm);
+                while (any) {
+                    const int j = __ffs(any) - 1;
+                    any &= any - 1;
+                    const int t = t0 + j;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, (pm >> j) & 1u);
+                    const uint32_t cl = __ballot_sync(0xffffffffu, (cm >> j) & 1u);
+                    if (lane == 0) {
+                        const uint32_t old = atomicOr(tb + (t >> 5), 1u << (t & 31));
+                        if (!((old >> (t & 31)) & 1u)) lst[atomicAdd(&nlist, 1)] = (uint16_t)t;
+                        atomicAdd(prio + t, (uint32_t)__popc(cl) * 256u + (uint32_t)__popc(bal));
+                    }
                 }
             }
         }
     }
     __syncthreads();
-    uint32_t *out = p.tile_bits + (size_t)blockIdx.x * twords;
-    for (int i = threadIdx.x; i < twords; i += FPC) out[i] = tb[i];
+    // best-first order for k_classify: tiles that contain more of the CTA's fibers (inside all
+    // three spheres) first, then tiles that more fibers may need, then the tile index.  Any order
+    // gives the same result (the (d^2, bundle) minimum is order-independent); a good order makes
+    // the running best tight early, which prunes the later tiles.
+    const int n = nlist;
+    int32_t *out = reinterpret_cast<int32_t *>(p.tile_bits) + (size_t)blockIdx.x * (p.T + 1);
+    if (threadIdx.x == 0) out[0] = n;
+    for (int i = threadIdx.x; i < n; i += FPC) {
+        const int ti = lst[i];
+        const uint32_t ki = prio[ti];
+        int rank = 0;
+        for (int k = 0; k < n; ++k) {
+            const int tk = lst[k];
+            const uint32_t kk = prio[tk];
+            rank += (kk > ki || (kk == ki && tk < ti)) ? 1 : 0;
+        }
+        out[1 + rank] = ti;
+    }
 }
 
 size_t classify_smem_bytes(int, int) { return SmemLayout().total; }
 
 int classify_fibers_per_cta() { return FPC; }
 
-size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)((T + 31) >> 5); }
+int classify_max_tiles() { return MAX_TILES; }
+
+size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(T + 1); }
 
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s) {
     if (p.n <= 0) return cudaSuccess;
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
-    const size_t cull_smem = sizeof(uint32_t) * (size_t)(((p.T + 31) >> 5) + ((p.B + 31) >> 5));
+    const size_t cull_smem = sizeof(uint32_t) * (size_t)(((p.T + 31) >> 5) + ((p.B + 31) >> 5) + p.T) +
+                             sizeof(uint16_t) * (size_t)p.T;
     cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
     if (e != cudaSuccess) return e;
     k_cull<<<grid, FPC, cull_smem, s>>>(p);

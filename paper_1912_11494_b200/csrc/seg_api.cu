@@ -337,6 +337,9 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
     Plan P;
     rc = make_plan(cents.data(), bid.data(), M, B, P);
     if (rc) return rc;
+    if (P.T > classify_max_tiles())
+        return fail(SEG_EINVAL, "seg_create: atlas needs " + std::to_string(P.T) + " tiles of 32 centroids; this build "
+                                "supports at most " + std::to_string(classify_max_tiles()));
 
     // device images
     std::vector<float4> tiles((size_t)P.T * TILE_STRIDE_F4);

@@ -48,7 +48,7 @@ struct ClassifyParams {
     const BundleHdr *bh;      // [B]
     int B, T;
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
-    uint32_t *tile_bits;       // [ceil(n / FPC)][ceil(T / 32)] scratch: k_cull -> k_classify
+    uint32_t *tile_bits;       // [ceil(n / FPC)][T + 1] scratch: k_cull -> k_classify ordered tile lists
 };
 
 struct MortonParams {
@@ -66,6 +66,7 @@ cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s);
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
+int classify_max_tiles();
 int classify_fibers_per_cta();
 
 }  // namespace seg
