@@ -37,6 +37,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -340,49 +344,47 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
     const bool inrange = consumer && gi < p.n;
     const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
     if (consumer) {
-        // this lane loads floats k0 = lane and k1 = 32 + lane (k1 < 63) of every fiber of the warp,
-        // 8 fibers per batch so 16 loads per lane are in flight before the first store
+        // every value straight from global into its shared-memory plane with 4-byte cp.async
+        // (LDGSTS): this lane copies floats k0 = lane and k1 = 32 + lane (k1 < 63) of each of the
+        // warp's 32 fibers, all in flight at once; then it checks the values it copied
         const int k0 = lane, k1 = 32 + lane;
-        const int p0 = k0 / 3, c0 = k0 % 3, p1 = k1 / 3, c1 = k1 % 3;
-        auto put = [&](int j, int pt, int c, float v) {
+        // plane of float k of a fiber: its address for fiber 0 of the warp and its stride in floats
+        auto plane = [&](int k, int &stride) -> float * {
             // fe = (x0, x20, y0, y20), fez = (z0, z20), fm = (x10, y10, z10, finite)
+            const int pt = k / 3, c = k % 3;
             if (pt == 0 || pt == 20) {
-                if (c < 2) reinterpret_cast<float *>(fe + j)[2 * c + (pt == 20 ? 1 : 0)] = v;
-                else reinterpret_cast<float *>(fez + j)[pt == 20 ? 1 : 0] = v;
-            } else if (pt == 10) {
-                reinterpret_cast<float *>(fm + j)[c] = v;
-            } else if (c < 2) {
-                reinterpret_cast<float *>(fxy + mid_slot(pt) * 32 + j)[c] = v;
-            } else {
-                fz[mid_slot(pt) * 32 + j] = v;
+                if (c < 2) { stride = 4; return reinterpret_cast<float *>(fe) + 2 * c + (pt == 20 ? 1 : 0); }
+                stride = 2;
+                return reinterpret_cast<float *>(fez) + (pt == 20 ? 1 : 0);
             }
+            if (pt == 10) { stride = 4; return reinterpret_cast<float *>(fm) + c; }
+            if (c < 2) { stride = 2; return reinterpret_cast<float *>(fxy + mid_slot(pt) * 32) + c; }
+            stride = 1;
+            return fz + mid_slot(pt) * 32;
         };
-        uint32_t fin = 0;   // bit j: this lane's two values of fiber j are finite
-        for (int jb = 0; jb < 32; jb += 8) {
-            float v0[8], v1[8];
-            int fjs[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int fj = __shfl_sync(0xffffffffu, fidx, jb + q);
-                fjs[q] = fj;
-                v0[q] = 0.f;
-                v1[q] = 0.f;
-                if (fj >= 0) {
-                    const float *src = p.fibers + (size_t)fj * (3 * NPTS);
-                    v0[q] = __ldg(src + k0);
-                    if (k1 < 3 * NPTS) v1[q] = __ldg(src + k1);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int j = jb + q;
-                if (isfinite(v0[q]) && isfinite(v1[q]) && fjs[q] >= 0) fin |= 1u << j;
-                put(j, p0, c0, v0[q]);
-                if (k1 < 3 * NPTS) put(j, p1, c1, v1[q]);
+        int s0 = 1, s1 = 1;
+        float *d0 = plane(k0, s0), *d1 = plane(k1 < 3 * NPTS ? k1 : 0, s1);
+        int fjs = -1;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            const int fj = __shfl_sync(0xffffffffu, fidx, j);
+            if (lane == j) fjs = fj;
+            if (fj >= 0) {
+                const float *src = p.fibers + (size_t)fj * (3 * NPTS);
+                cp_async4(d0 + j * s0, src + k0);
+                if (k1 < 3 * NPTS) cp_async4(d1 + j * s1, src + k1);
             }
         }
+        cp_async_wait_all();
+        uint32_t fin = 0;   // bit j: this lane's two values of fiber j are finite
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            const bool ok = isfinite(d0[j * s0]) && (k1 >= 3 * NPTS || isfinite(d1[j * s1]));
+            fin |= (ok ? 1u : 0u) << j;
+        }
         fin = __reduce_and_sync(0xffffffffu, fin);   // bit j: every value of fiber j is finite
-        fm[lane].w = ((fin >> lane) & 1u) ? 1.f : 0.f;
+        __syncwarp();
+        fm[lane].w = (((fin >> lane) & 1u) && fjs >= 0) ? 1.f : 0.f;
         best[lane] = (p.seed && inrange) ? p.seed[fidx] : KEY_NONE;
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
@@ -530,6 +532,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
                     hit = __reduce_or_sync(0xffffffffu, hit);
+#if defined(SEG_EXP) && SEG_EXP == 3
+                    hit = p.n < 0 ? hit : 0;  // experiment: dense test1+test2 only (opaque, so it is not dead code)
+#endif
                     if (!hit) continue;
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {

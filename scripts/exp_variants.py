@@ -10,7 +10,7 @@ from synth import atlas_for_config, fibers_for_config
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 variants = {0: _build.LIB}
 os.makedirs("build/exp", exist_ok=True)
-for k in (1, 2):
+for k in (1, 2, 3):
     out = f"build/exp/libseg_exp{k}.so"
     subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, f"-DSEG_EXP={k}", "-o", out, *_build.SOURCES],
                           stderr=subprocess.DEVNULL)
@@ -34,4 +34,4 @@ for k, path in variants.items():
     torch.cuda.synchronize(); e0.record()
     for _ in range(10): f()
     e1.record(); torch.cuda.synchronize()
-    print(f"cfg{cfg} variant {k}: {e0.elapsed_time(e1)/10:.3f} ms  ({['production','tile-loop only','no candidate rounds'][k]})")
+    print(f"cfg{cfg} variant {k}: {e0.elapsed_time(e1)/10:.3f} ms  ({['production','tile-loop only','no candidate rounds','dense only (no hit processing)'][k]})")
