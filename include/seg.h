@@ -144,14 +144,15 @@ int seg_plan_tiles(const float *centroids, const int32_t *bundle_id, int64_t M, 
  * Profiling hook (bench.py only; NOT thread-safe, unlike the rest of the context):
  * after seg_profile_enable(atlas, cap) the first `cap` device-pointer seg_classify calls
  * on `atlas` record CUDA events on their stream before the spatial prepass, before the
- * classify kernel and after it.  seg_profile_read synchronises on those events and writes,
- * per recorded call i < min(count, capacity), prepass_ms[i] and classify_ms[i] (host arrays);
+ * tile-list kernel (k_cull), before the classify kernel and after it.  seg_profile_read
+ * synchronises on those events and writes, per recorded call i < min(count, capacity),
+ * prepass_ms[i], cull_ms[i] and classify_ms[i] (nullable host arrays);
  * *count receives the number of recorded calls.  cap = 0 disables and frees the events.
  * Errors: SEG_EINVAL (null atlas, cap < 0), SEG_ECUDA.
  */
 int seg_profile_enable(seg_atlas *atlas, int32_t capacity);
-int seg_profile_read(seg_atlas *atlas, float *prepass_ms, float *classify_ms, int32_t capacity,
-                     int32_t *count);
+int seg_profile_read(seg_atlas *atlas, float *prepass_ms, float *cull_ms, float *classify_ms,
+                     int32_t capacity, int32_t *count);
 
 /*
  * seg_debug_classify_seeded -- experiment hook (device pointers only): seg_classify with each

@@ -54,7 +54,7 @@ def _load() -> ctypes.CDLL:
     lib.seg_profile_enable.restype = ctypes.c_int
     lib.seg_profile_enable.argtypes = [vp, i32]
     lib.seg_profile_read.restype = ctypes.c_int
-    lib.seg_profile_read.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    lib.seg_profile_read.argtypes = [vp, vp, vp, vp, i32, ctypes.POINTER(i32)]
     lib.seg_destroy.restype = None
     lib.seg_destroy.argtypes = [vp]
     lib.seg_last_error.restype = ctypes.c_char_p
@@ -129,9 +129,10 @@ def seg_profile_enable(atlas: int, capacity: int) -> None:
     _check(LIB.seg_profile_enable(atlas, int(capacity)))
 
 
-def seg_profile_read(atlas: int, prepass_ms, classify_ms, capacity: int) -> int:
+def seg_profile_read(atlas: int, prepass_ms, cull_ms, classify_ms, capacity: int) -> int:
     cnt = ctypes.c_int32()
-    _check(LIB.seg_profile_read(atlas, _ptr(prepass_ms), _ptr(classify_ms), int(capacity), ctypes.byref(cnt)))
+    _check(LIB.seg_profile_read(atlas, _ptr(prepass_ms), _ptr(cull_ms), _ptr(classify_ms), int(capacity),
+                                ctypes.byref(cnt)))
     return cnt.value
 
 

@@ -121,18 +121,31 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 6 bits -> every th
     return v;
 }
 
+constexpr int MORTON_FPT = 4;   // fibers per thread in k_morton_hist (independent loads in flight)
+
 __global__ void k_morton_hist(MortonParams p) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
-    const float *f = p.fibers + (size_t)i * (3 * NPTS) + 30;  // point 10
     const float lim = (float)((1 << MORTON_BITS) - 1);
-    // fmaxf/fminf map NaN to the bound, so non-finite fibers land in a valid bucket
-    const float qx = fminf(fmaxf((__ldg(f + 0) - p.lo.x) * p.inv_cell.x, 0.f), lim);
-    const float qy = fminf(fmaxf((__ldg(f + 1) - p.lo.y) * p.inv_cell.y, 0.f), lim);
-    const float qz = fminf(fmaxf((__ldg(f + 2) - p.lo.z) * p.inv_cell.z, 0.f), lim);
-    const uint32_t k = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
-    p.key[i] = k;
-    atomicAdd(p.hist + k, 1u);
+    const int i0 = blockIdx.x * blockDim.x * MORTON_FPT + threadIdx.x;
+    float v[MORTON_FPT][3];
+#pragma unroll
+    for (int q = 0; q < MORTON_FPT; ++q) {
+        const int i = i0 + q * blockDim.x;
+        const float *f = p.fibers + (size_t)min(i, p.n - 1) * (3 * NPTS) + 30;  // point 10
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[q][c] = __ldg(f + c);
+    }
+#pragma unroll
+    for (int q = 0; q < MORTON_FPT; ++q) {
+        const int i = i0 + q * blockDim.x;
+        if (i >= p.n) break;
+        // fmaxf/fminf map NaN to the bound, so non-finite fibers land in a valid bucket
+        const float qx = fminf(fmaxf((v[q][0] - p.lo.x) * p.inv_cell.x, 0.f), lim);
+        const float qy = fminf(fmaxf((v[q][1] - p.lo.y) * p.inv_cell.y, 0.f), lim);
+        const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * p.inv_cell.z, 0.f), lim);
+        const uint32_t k = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
+        p.key[i] = k;
+        atomicAdd(p.hist + k, 1u);
+    }
 }
 
 // In-place exclusive scan of MORTON_BUCKETS counters by one CTA of 1024 threads, 4 per thread per
@@ -184,7 +197,7 @@ cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * MORTON_BUCKETS, s);
     if (e != cudaSuccess) return e;
     const int g = (p.n + 255) / 256;
-    k_morton_hist<<<g, 256, 0, s>>>(p);
+    k_morton_hist<<<(p.n + 256 * MORTON_FPT - 1) / (256 * MORTON_FPT), 256, 0, s>>>(p);
     k_scan_exclusive<<<1, 1024, 0, s>>>(p.hist);
     k_morton_scatter<<<g, 256, 0, s>>>(p);
     return cudaGetLastError();
@@ -616,20 +629,24 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
 // latency-bound header loads run at full occupancy.
 // ----------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
-    // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list, count
+    // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list (u16)
     extern __shared__ uint32_t sbits[];
     const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
     uint32_t *tb = sbits, *bb = sbits + twords, *prio = bb + bwords;
     uint16_t *lst = reinterpret_cast<uint16_t *>(prio + p.T);
     __shared__ int nlist;
-    __shared__ BundleHdr sbh[MAX_SMEM_BUNDLES];
+    // per bundle the point-10 sphere grown by the bundle threshold: (centre, R); an empty bundle gets a
+    // centre at 1e30 so that no fiber passes it
+    __shared__ float4 sbs[MAX_SMEM_BUNDLES];
     for (int i = threadIdx.x; i < twords + bwords + p.T; i += FPC) sbits[i] = 0;
-    if (threadIdx.x == 0) nlist = 0;
-    // bundle headers staged once per CTA (broadcast reads below) when they fit
     const bool stage_bh = p.B <= MAX_SMEM_BUNDLES;
+    auto bsphere = [&](int b) {
+        const BundleHdr h = p.bh[b];
+        return h.t1 > h.t0 ? make_float4(h.s10.x, h.s10.y, h.s10.z, h.s10.w + h.thr + CULL_EPS)
+                           : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+    };
     if (stage_bh)
-        for (int i = threadIdx.x; i < p.B; i += FPC) sbh[i] = p.bh[i];
-    const BundleHdr *bhp = stage_bh ? sbh : p.bh;
+        for (int i = threadIdx.x; i < p.B; i += FPC) sbs[i] = bsphere(i);
     const int lane = threadIdx.x & 31;
     const int gi = blockIdx.x * FPC + threadIdx.x;
     bool ok = gi < p.n;
@@ -645,16 +662,15 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
              isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
     }
     __syncthreads();
+    // bundles some fiber of the CTA may need (point-10 sphere + threshold, exact)
     for (int b0 = 0; b0 < p.B; b0 += 32) {
         uint32_t m = 0;
-#pragma unroll 4
+#pragma unroll 8
         for (int j = 0; j < 32; ++j) {
             const int b = b0 + j;
             if (b < p.B) {
-                const BundleHdr h = bhp[b];
-                const float r = h.s10.w + h.thr + CULL_EPS;
-                const bool pass = ok && h.t1 > h.t0 && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
-                m |= (pass ? 1u : 0u) << j;
+                const float4 c = stage_bh ? sbs[b] : bsphere(b);
+                m |= ((ok && d2(F10.x, F10.y, F10.z, c) <= c.w * c.w) ? 1u : 0u) << j;
             }
         }
         m = __reduce_or_sync(0xffffffffu, m);
@@ -666,13 +682,13 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         while (bits) {
             const int b = (w << 5) + __ffs(bits) - 1;
             bits &= bits - 1;
-            const BundleHdr h = bhp[b];
-            const float sv = h.thr + CULL_EPS;
-            const float r = h.s10.w + sv;
-            const bool bpass = ok && d2(F10.x, F10.y, F10.z, h.s10) <= r * r;
+            const float4 c = stage_bh ? sbs[b] : bsphere(b);
+            const bool bpass = ok && d2(F10.x, F10.y, F10.z, c) <= c.w * c.w;
             if (!__any_sync(0xffffffffu, bpass)) continue;
+            const BundleHdr h = p.bh[b];
+            const float sv = h.thr + CULL_EPS;
             for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
-                // 32 tiles per chunk: independent header loads and tests (ILP), then bookkeeping
+                // 32 tiles per chunk: independent header loads and tests (ILP)
                 const int nt = min(32, h.t1 - t0);
                 uint32_t pm = 0, cm = 0;
 #pragma unroll 4
@@ -687,21 +703,47 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
                         cm |= (close ? 1u : 0u) << j;
                     }
                 }
+                // transpose: lane j gets the pass / inside counts of tile t0 + j over the warp,
+                // then every lane records its own tile (parallel shared atomics)
                 uint32_t any = __reduce_or_sync(0xffffffffu, pm);
+                int npass = 0, nclose = 0;
                 while (any) {
                     const int j = __ffs(any) - 1;
                     any &= any - 1;
-                    const int t = t0 + j;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, (pm >> j) & 1u);
-                    const uint32_t cl = __ballot_sync(0xffffffffu, (cm >> j) & 1u);
-                    if (lane == 0) {
-                        const uint32_t old = atomicOr(tb + (t >> 5), 1u << (t & 31));
-                        if (!((old >> (t & 31)) & 1u)) lst[atomicAdd(&nlist, 1)] = (uint16_t)t;
-                        atomicAdd(prio + t, (uint32_t)__popc(cl) * 256u + (uint32_t)__popc(bal));
-                    }
+                    const int a = __popc(__ballot_sync(0xffffffffu, (pm >> j) & 1u));
+                    const int c2 = __popc(__ballot_sync(0xffffffffu, (cm >> j) & 1u));
+                    if (lane == j) { npass = a; nclose = c2; }
+                }
+                if (npass) {
+                    const int t = t0 + lane;
+                    atomicOr(tb + (t >> 5), 1u << (t & 31));
+                    atomicAdd(prio + t, (uint32_t)nclose * 256u + (uint32_t)npass);
                 }
             }
         }
+    }
+    __syncthreads();
+    // the CTA's tiles from the bit set (warp 0: prefix over the words), in tile order
+    if (threadIdx.x < 32) {
+        int base = 0;
+        for (int w0 = 0; w0 < twords; w0 += 32) {
+            const uint32_t bits = w0 + lane < twords ? tb[w0 + lane] : 0u;
+            const int c = __popc(bits);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int pos = base + incl - c;
+            uint32_t bb2 = bits;
+            while (bb2) {
+                lst[pos++] = (uint16_t)(((w0 + lane) << 5) + __ffs(bb2) - 1);
+                bb2 &= bb2 - 1;
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) nlist = base;
     }
     __syncthreads();
     // best-first order for k_classify: tiles that contain more of the CTA's fibers (inside all
@@ -732,7 +774,7 @@ int classify_max_tiles() { return MAX_TILES; }
 
 size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(T + 1); }
 
-cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s) {
+cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull) {
     if (p.n <= 0) return cudaSuccess;
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
@@ -741,6 +783,10 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s)
     cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
     if (e != cudaSuccess) return e;
     k_cull<<<grid, FPC, cull_smem, s>>>(p);
+    if (after_cull) {
+        e = cudaEventRecord(after_cull, s);
+        if (e != cudaSuccess) return e;
+    }
     if (stats) {
         e = cudaFuncSetAttribute(k_classify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -51,7 +51,7 @@ struct seg_atlas {
     float3 lo{}, inv_cell{};      // Morton grid of the prepass
     int64_t bytes = 0;
     // profiling hook (seg_profile_enable / seg_profile_read); mutable, not thread-safe
-    mutable std::vector<cudaEvent_t> prof_ev;  // 3 per recorded call
+    mutable std::vector<cudaEvent_t> prof_ev;  // 4 per recorded call
     mutable int prof_cap = 0, prof_n = 0;
 };
 
@@ -451,7 +451,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
                     unsigned long long *d_stats, const unsigned long long *seed = nullptr) {
     if (n == 0) return SEG_OK;
     cudaEvent_t *ev = nullptr;
-    if (a->prof_n < a->prof_cap) ev = &a->prof_ev[3 * (a->prof_n++)];
+    if (a->prof_n < a->prof_cap) ev = &a->prof_ev[4 * (a->prof_n++)];
     if (ev) SEG_CUDA(cudaEventRecord(ev[0], s), "seg_classify: profile event");
     uint32_t *key = nullptr, *hist = nullptr;
     int32_t *perm = nullptr;
@@ -468,8 +468,8 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
              "seg_classify: cudaMallocAsync");
     ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
-    cudaError_t e = launch_classify(cp, d_stats != nullptr, s);
-    if (ev && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
+    cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
+    if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
     cudaFreeAsync(tbits, s);
     if (key) {
         cudaFreeAsync(key, s);
@@ -618,7 +618,7 @@ extern "C" int seg_profile_enable(seg_atlas *a, int32_t cap) {
     free_prof(a);
     if (cap == 0) return SEG_OK;
     try {
-        a->prof_ev.resize((size_t)3 * cap);
+        a->prof_ev.resize((size_t)4 * cap);
     } catch (const std::bad_alloc &) {
         return fail(SEG_ENOMEM, "seg_profile_enable: host allocation failed");
     }
@@ -635,19 +635,23 @@ extern "C" int seg_profile_enable(seg_atlas *a, int32_t cap) {
     return SEG_OK;
 }
 
-extern "C" int seg_profile_read(seg_atlas *a, float *prepass_ms, float *classify_ms, int32_t cap, int32_t *count) {
+extern "C" int seg_profile_read(seg_atlas *a, float *prepass_ms, float *cull_ms, float *classify_ms, int32_t cap,
+                                int32_t *count) {
     if (!a || !count) return fail(SEG_EINVAL, "seg_profile_read: null pointer");
     DeviceGuard guard(a->device);
     *count = a->prof_n;
     const int n = std::min(a->prof_n, std::max(0, (int)cap));
     for (int i = 0; i < n; ++i) {
-        cudaEvent_t *ev = &a->prof_ev[3 * i];
-        SEG_CUDA(cudaEventSynchronize(ev[2]), "seg_profile_read: cudaEventSynchronize");
+        cudaEvent_t *ev = &a->prof_ev[4 * i];
+        SEG_CUDA(cudaEventSynchronize(ev[3]), "seg_profile_read: cudaEventSynchronize");
+        float t2 = 0.f;
+        SEG_CUDA(cudaEventElapsedTime(&t2, ev[2], ev[3]), "seg_profile_read: elapsed");
         float t0 = 0.f, t1 = 0.f;
         SEG_CUDA(cudaEventElapsedTime(&t0, ev[0], ev[1]), "seg_profile_read: elapsed");
         SEG_CUDA(cudaEventElapsedTime(&t1, ev[1], ev[2]), "seg_profile_read: elapsed");
         if (prepass_ms) prepass_ms[i] = t0;
-        if (classify_ms) classify_ms[i] = t1;
+        if (cull_ms) cull_ms[i] = t1;
+        if (classify_ms) classify_ms[i] = t2;
     }
     return SEG_OK;
 }

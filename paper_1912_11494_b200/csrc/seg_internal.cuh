@@ -63,7 +63,7 @@ struct MortonParams {
 
 // Launchers (classify.cu).  All are asynchronous on `s`.
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
-cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s);
+cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull = nullptr);
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
 int classify_max_tiles();

@@ -3,5 +3,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1500 python -m pytest tests -x -q -m gpu -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -4 gpurun_out/pytest_gpu.log | grep -v Warning
 timeout 600 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo bench_rc=$?
-tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ms/step', d['ms_per_step'], 'kernel_ms', d['roofline']['kernel_ms'], 'frac', d['roofline']['frac']); print(d['cascade'])"
+python scripts/bench_brief.py gpurun_out/bench.log
 timeout 300 python scripts/stats_cfg.py 3 > gpurun_out/stats3.log 2>&1; tail -1 gpurun_out/stats3.log | cut -c1-1500
