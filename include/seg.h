@@ -96,7 +96,7 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
                  int32_t *label, float *dist, void *stream);
 
 /* Number of counters written by seg_classify_stats. */
-#define SEG_NSTATS 12
+#define SEG_NSTATS 17
 /*
  * seg_classify_stats -- seg_classify (device pointers only) with the kernel's
  * per-stage counters (SPEC.md:233-236 CascadeStats, extended), accumulated into the
@@ -108,6 +108,9 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
  *   [7] lane full 21-point completions               [8] best-distance updates (Alg. 1 l.15-16)
  *   [9] lane point-distance evaluations (Eq. 1, all stages and the sphere bounds)
  *   [10] lane sphere-bound tests (bundle + tile)     [11] CTAs
+ *   clock64 cycles summed over consumer warps: [12] tile loop, [13] waiting for a tile,
+ *   [14] best-first candidate selection (incl. the candidate rounds it triggers),
+ *   [15] candidate rounds, [16] live tile-bound test
  * A separate kernel instantiation; it computes the same labels and distances.
  */
 int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,

@@ -13,10 +13,11 @@ from . import _build
 
 SEG_OK, SEG_EINVAL, SEG_ENOMEM, SEG_ECUDA = 0, -1, -2, -3
 SEG_NPTS = 21
-SEG_NSTATS = 12
+SEG_NSTATS = 17
 STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_pass", "lane_test1",
               "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
-              "lane_sphere_tests", "ctas")
+              "lane_sphere_tests", "ctas",
+              "cyc_consumer", "cyc_full_wait", "cyc_hit_select", "cyc_cand_rounds", "cyc_tile_test")
 
 
 class SegError(RuntimeError):

@@ -241,7 +241,7 @@ constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle h
 
 enum {
     ST_FIBERS = 0, ST_WT_LISTED, ST_WT_COMPUTED, ST_LT_PASS, ST_T1, ST_T2, ST_T34, ST_FULL, ST_UPD,
-    ST_PDIST, ST_SPHERE, ST_CTAS, ST_N
+    ST_PDIST, ST_SPHERE, ST_CTAS, ST_CYC_CONS, ST_CYC_FULLWAIT, ST_CYC_HIT, ST_CYC_FLUSH, ST_CYC_SPHERE, ST_N
 };
 
 struct StageMeta {
@@ -428,18 +428,26 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
         const float4 myE = fe[lane], myF10 = fm[lane];
         const float2 myEz = fez[lane];
         const bool myok = myF10.w != 0.f;
+        long long tc0 = 0;
+        if (STATS) tc0 = clock64();
         for (int k = 0;; ++k) {
             const int s = k % STAGES, u = k / STAGES;
+            long long tw0 = 0;
+            if (STATS) tw0 = clock64();
             mbar_sleep_wait(full + s, u & 1);
+            if (STATS && lane == 0) cnt[ST_CYC_FULLWAIT] += clock64() - tw0;
             if (meta[s].tile < 0) break;
             const float4 *stage = ring + s * TILE_STRIDE_F4;
             const TileHdr th = *reinterpret_cast<const TileHdr *>(stage);
             const float thr2 = th.thr2;
             const int b = th.bundle;
+            long long ts0 = 0;
+            if (STATS) ts0 = clock64();
             const float tau = fminf(thr2, key_d2(best[lane]));
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
             const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sqrtf(tau) + CULL_EPS);
             uint32_t pm = __ballot_sync(0xffffffffu, pass);
+            if (STATS && lane == 0) cnt[ST_CYC_SPHERE] += clock64() - ts0;
 #if defined(SEG_EXP) && SEG_EXP == 1
             pm = 0;  // experiment: tile loop overhead only
 #endif
@@ -504,6 +512,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                 };
                 int np = 0, n2 = 0;
                 auto flush = [&](int keep) {   // best-first: the per-fiber winners, then the rest
+                    long long tf0 = 0;
+                    if (STATS) tf0 = clock64();
                     __syncwarp();
                     if (np) run_cand(pe, pr, np);
                     np = 0;
@@ -512,6 +522,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         n2 -= m;
                         run_cand(q2e + n2, q2r + n2, m);
                     }
+                    if (STATS && lane == 0) cnt[ST_CYC_FLUSH] += clock64() - tf0;
                 };
                 // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
                 const float4 c10 = T[10 * TILE + lane];
@@ -549,6 +560,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                     hit = p.n < 0 ? hit : 0;  // experiment: dense test1+test2 only (opaque, so it is not dead code)
 #endif
                     if (!hit) continue;
+                    long long th0 = 0;
+                    if (STATS) th0 = clock64();
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         if (!((hit >> q) & 1u)) continue;
@@ -584,6 +597,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         n2 += __popc(bd) + __popc(bi);
                         if (n2 > Q2CAP - 64) flush(31);
                     }
+                    if (STATS && lane == 0) cnt[ST_CYC_HIT] += clock64() - th0;
                 }
                 flush(0);
             }
@@ -591,6 +605,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
             if (lane == 0) mbar_arrive(empty + s);
         }
 
+        if (STATS && lane == 0) cnt[ST_CYC_CONS] += clock64() - tc0;
         // ---- a8: epilogue ----
         if (inrange) {
             const unsigned long long key = best[lane];
