@@ -227,11 +227,16 @@ cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
 //       64-bit atomicMin (lexicographic, so tile order and orientation never matter);
 //   a8  epilogue: label / sqrt(d^2) stored through the permutation.
 // ----------------------------------------------------------------------------------------
-constexpr int NCW = 8;                 // consumer warps
+constexpr int NCW = 8;                 // consumer warps (4 warps x 3 CTAs/SM measured slower: 8.74 vs 7.73 ms)
+constexpr int CTAS_PER_SM = 2;
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
 constexpr int STAGES = 3;              // tile ring depth
+#if defined(SEG_FB8)
+constexpr int FB = 8;
+#else
 constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop
+#endif
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
@@ -249,8 +254,9 @@ struct StageMeta {
 };
 
 struct SmemLayout {
-    size_t ring, fxy, fz, fe, fez, fm, pe, pr, q2e, q2r, best, bars, meta, total;
-    __host__ __device__ SmemLayout() {
+    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, pe = 0, pr = 0, q2e = 0, q2r = 0, best = 0, bars = 0,
+           meta = 0, total = 0;
+    __host__ __device__ constexpr SmemLayout() {
         size_t o = 0;
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
         fxy = o;  o += (size_t)NCW * NMID * 32 * sizeof(float2);
@@ -269,10 +275,17 @@ struct SmemLayout {
     }
 };
 
+// CTAS_PER_SM CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
+static_assert(SmemLayout().total <= 233472 / CTAS_PER_SM - 1024, "k_classify shared memory exceeds the CTA/SM budget");
+
 // plane slot of fiber point i (i != 0, 10, 20)
 __host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
 
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) {
+#if defined(SEG_SPIN)
+    mbar_wait(bar, parity);
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAITS_%=:\n\t"
@@ -312,7 +325,7 @@ __device__ __forceinline__ bool tile_pass_inside(const float4 &E, const float2 &
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
+__global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemLayout L;
     float4 *ring = reinterpret_cast<float4 *>(smem + L.ring);
@@ -428,6 +441,74 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
         const float4 myE = fe[lane], myF10 = fm[lane];
         const float2 myEz = fez[lane];
         const bool myok = myF10.w != 0.f;
+        // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
+        // starting from its 3-point running max r
+        auto run_cand = [&](const uint32_t *qe, const float *qr, int n) {
+#if defined(SEG_EXP) && SEG_EXP == 2
+            n = 0;  // experiment: no candidate rounds
+#endif
+            if (lane < n) {
+                const uint32_t e = qe[lane];
+                float r = qr[lane];
+                const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1, es = (e >> 11) & 3;
+                // the candidate's tile: the ring stage recorded in its entry
+                const float4 *estage = ring + es * TILE_STRIDE_F4;
+                const float4 *T = estage + TILE_HDR_F4;
+                const float thr2 = reinterpret_cast<const TileHdr *>(estage)->thr2;
+                const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
+                const float taul = fminf(thr2, key_d2(best[fl]));
+                if (r <= taul) {  // re-check against the freshest best (best-first pays here)
+                    const float4 *cb = T + c + (o ? 20 * TILE : 0);
+                    const int st = o ? -TILE : TILE;
+                    bool done = false;
+#define SEG_STEP(i)                                                             \
+    {                                                                           \
+const float2 a = fxy[mid_slot(i) * 32 + fl];                            \
+r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
+    }
+                    if (STATS) cnt[ST_T34]++;
+                    SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
+                    if (STATS) cnt[ST_PDIST] += 4;
+                    if (r > taul) done = true;
+                    if (!done) {
+                        SEG_STEP(1); SEG_STEP(19); SEG_STEP(5); SEG_STEP(15);
+                        if (STATS) cnt[ST_PDIST] += 4;
+                        if (r > taul) done = true;
+                    }
+                    if (!done) {
+                        SEG_STEP(2); SEG_STEP(18); SEG_STEP(4); SEG_STEP(16);
+                        if (STATS) cnt[ST_PDIST] += 4;
+                        if (r > taul) done = true;
+                    }
+                    if (!done) {
+                        SEG_STEP(6); SEG_STEP(14); SEG_STEP(8); SEG_STEP(12); SEG_STEP(9);
+                        SEG_STEP(11);
+                        if (STATS) { cnt[ST_PDIST] += 6; cnt[ST_FULL]++; }
+                        // a7: lexicographic (d^2, bundle) minimum
+                        if (r <= thr2) {
+                            atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
+                            if (STATS) cnt[ST_UPD]++;
+                        }
+                    }
+#undef SEG_STEP
+                }
+            }
+            __syncwarp();
+        };
+        int np = 0, n2 = 0;
+        auto flush = [&](int keep) {   // best-first: the per-fiber winners, then the rest
+            long long tf0 = 0;
+            if (STATS) tf0 = clock64();
+            __syncwarp();
+            if (np) run_cand(pe, pr, np);
+            np = 0;
+            while (n2 > keep) {
+                const int m = n2 >= 32 ? 32 : n2;
+                n2 -= m;
+                run_cand(q2e + n2, q2r + n2, m);
+            }
+            if (STATS && lane == 0) cnt[ST_CYC_FLUSH] += clock64() - tf0;
+        };
         long long tc0 = 0;
         if (STATS) tc0 = clock64();
         for (int k = 0;; ++k) {
@@ -461,69 +542,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                     if (lane == 0) cnt[ST_WT_COMPUTED]++;
                     if ((pm >> lane) & 1u) { cnt[ST_LT_PASS]++; cnt[ST_T1] += TILE; cnt[ST_PDIST] += TILE; }
                 }
-                // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
-                // starting from its 3-point running max r
-                auto run_cand = [&](const uint32_t *qe, const float *qr, int n) {
-#if defined(SEG_EXP) && SEG_EXP == 2
-                    n = 0;  // experiment: no candidate rounds
-#endif
-                    if (lane < n) {
-                        const uint32_t e = qe[lane];
-                        float r = qr[lane];
-                        const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1;
-                        const float taul = fminf(thr2, key_d2(best[fl]));
-                        if (r <= taul) {  // re-check against the freshest best (best-first pays here)
-                            const float4 *cb = T + c + (o ? 20 * TILE : 0);
-                            const int st = o ? -TILE : TILE;
-                            bool done = false;
-#define SEG_STEP(i)                                                             \
-    {                                                                           \
-        const float2 a = fxy[mid_slot(i) * 32 + fl];                            \
-        r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
-    }
-                            if (STATS) cnt[ST_T34]++;
-                            SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
-                            if (STATS) cnt[ST_PDIST] += 4;
-                            if (r > taul) done = true;
-                            if (!done) {
-                                SEG_STEP(1); SEG_STEP(19); SEG_STEP(5); SEG_STEP(15);
-                                if (STATS) cnt[ST_PDIST] += 4;
-                                if (r > taul) done = true;
-                            }
-                            if (!done) {
-                                SEG_STEP(2); SEG_STEP(18); SEG_STEP(4); SEG_STEP(16);
-                                if (STATS) cnt[ST_PDIST] += 4;
-                                if (r > taul) done = true;
-                            }
-                            if (!done) {
-                                SEG_STEP(6); SEG_STEP(14); SEG_STEP(8); SEG_STEP(12); SEG_STEP(9);
-                                SEG_STEP(11);
-                                if (STATS) { cnt[ST_PDIST] += 6; cnt[ST_FULL]++; }
-                                // a7: lexicographic (d^2, bundle) minimum
-                                if (r <= thr2) {
-                                    atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
-                                    if (STATS) cnt[ST_UPD]++;
-                                }
-                            }
-#undef SEG_STEP
-                        }
-                    }
-                    __syncwarp();
-                };
-                int np = 0, n2 = 0;
-                auto flush = [&](int keep) {   // best-first: the per-fiber winners, then the rest
-                    long long tf0 = 0;
-                    if (STATS) tf0 = clock64();
-                    __syncwarp();
-                    if (np) run_cand(pe, pr, np);
-                    np = 0;
-                    while (n2 > keep) {
-                        const int m = n2 >= 32 ? 32 : n2;
-                        n2 -= m;
-                        run_cand(q2e + n2, q2r + n2, m);
-                    }
-                    if (STATS && lane == 0) cnt[ST_CYC_FLUSH] += clock64() - tf0;
-                };
                 // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
                 const float4 c10 = T[10 * TILE + lane];
                 const float4 c0 = T[lane], c20 = T[20 * TILE + lane];
@@ -537,6 +555,37 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         jj[q] = pm ? __ffs(pm) - 1 : -1;
                         pm &= pm - 1;
                     }
+#if defined(SEG_T2SKIP)
+                    // test1 first; a fiber no lane passes skips test2 (warp-uniform branch)
+                    float m10q[FB], tjq[FB];
+                    uint32_t any1 = 0;
+#pragma unroll
+                    for (int q = 0; q < FB; ++q) {
+                        const int j = jj[q] < 0 ? 0 : jj[q];
+                        const float4 a10 = fm[j];
+                        tjq[q] = __shfl_sync(0xffffffffu, tau, j);
+                        m10q[q] = d2(a10.x, a10.y, a10.z, c10);
+                        if (jj[q] >= 0 && m10q[q] <= tjq[q]) any1 |= 1u << q;
+                    }
+                    any1 = __reduce_or_sync(0xffffffffu, any1);
+#pragma unroll
+                    for (int q = 0; q < FB; ++q) {
+                        rdv[q] = riv[q] = INFINITY;
+                        tjv[q] = tjq[q];
+                        if ((any1 >> q) & 1u) {
+                            const int j = jj[q];
+                            const float4 E = fe[j];
+                            const float2 Ez = fez[j];
+                            const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)), EZ = f2u(Ez);
+                            const float2 R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);
+                            const float2 R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);
+                            rdv[q] = fmaxf(fmaxf(m10q[q], R0.x), R20.y);
+                            riv[q] = fmaxf(fmaxf(m10q[q], R20.x), R0.y);
+                            if (fminf(rdv[q], riv[q]) <= tjq[q]) hit |= 1u << q;
+                        }
+                        if (STATS && jj[q] >= 0 && m10q[q] <= tjq[q]) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
+                    }
+#else
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         const int j = jj[q] < 0 ? 0 : jj[q];
@@ -555,6 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         if (jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj) hit |= 1u << q;
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
+#endif
                     hit = __reduce_or_sync(0xffffffffu, hit);
 #if defined(SEG_EXP) && SEG_EXP == 3
                     hit = p.n < 0 ? hit : 0;  // experiment: dense test1+test2 only (opaque, so it is not dead code)
@@ -576,7 +626,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                         const int wl = __ffs(__ballot_sync(0xffffffffu, sb == smin)) - 1;
                         const bool win = lane == wl;
                         const int wo = (ad && rd == sc) ? 0 : 1;
-                        const uint32_t e = (uint32_t)((j << 5) | lane);
+                        const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
                         if (win) {
                             pe[np] = e | ((uint32_t)wo << 10);
                             pr[np] = sc;
@@ -599,8 +649,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_classify(ClassifyParams p) {
                     }
                     if (STATS && lane == 0) cnt[ST_CYC_HIT] += clock64() - th0;
                 }
-                flush(0);
             }
+            flush(0);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
