@@ -480,18 +480,27 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     return SEG_OK;
 }
 
-// Host pointers: chunked H2D -> classify -> D2H, double-buffered over two streams.
+// Host pointers: chunked H2D -> classify -> D2H over three streams (copy-in, the caller's stream
+// for the kernels, copy-out) and NB device buffer sets, so that the host->device copy of chunk c+1
+// runs while chunk c is classified and chunk c-1 is copied back.  Buffer set i is reused by chunk
+// c + NB only after classify(c) has read its fibers (H2D waits on done[i]) and D2H(c) has read its
+// results (classify waits on out[i]).  Synchronous: returns when every result is on the host.
 int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab, float *dist, cudaStream_t s) {
-    constexpr int64_t CH = 1 << 19;  // fibers per chunk (126 MB)
+    constexpr int64_t CH = 1 << 18;  // fibers per chunk (63 MB): the non-overlapped tail is one chunk
+    constexpr int NBMAX = 3;
     const int64_t nchunks = (N + CH - 1) / CH;
-    const int nb = nchunks > 1 ? 2 : 1;
+    const int nb = (int)std::min<int64_t>(NBMAX, nchunks);
     const int64_t cap = std::min<int64_t>(N, CH);
-    cudaStream_t cs = nullptr;
-    SEG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "seg_classify: cudaStreamCreate");
-    cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
-    float *dfib[2] = {};
-    int32_t *dlab[2] = {};
-    float *ddist[2] = {};
+    cudaStream_t cin = nullptr, cout = nullptr;
+    SEG_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking), "seg_classify: cudaStreamCreate");
+    if (cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(cin);
+        return cuda_fail(cudaGetLastError(), "seg_classify: cudaStreamCreate");
+    }
+    cudaEvent_t ev_in[NBMAX] = {}, ev_done[NBMAX] = {}, ev_out[NBMAX] = {};
+    float *dfib[NBMAX] = {};
+    int32_t *dlab[NBMAX] = {};
+    float *ddist[NBMAX] = {};
     int rc = SEG_OK;
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < nb && e == cudaSuccess; ++i) {
@@ -502,36 +511,40 @@ int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab,
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
     }
-    // the copy stream must see the allocations made on s
+    // the copy streams must see the allocations made on s
     cudaEvent_t ev_alloc = nullptr;
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(ev_alloc, s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_alloc, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cin, ev_alloc, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cout, ev_alloc, 0);
     for (int64_t c = 0; c < nchunks && e == cudaSuccess && rc == SEG_OK; ++c) {
         const int i = (int)(c % nb);
         const int64_t lo = c * CH, n = std::min(CH, N - lo);
-        if (c >= nb) e = cudaStreamWaitEvent(cs, ev_out[i], 0);  // buffer i free (its D2H done)
+        if (c >= nb) e = cudaStreamWaitEvent(cin, ev_done[i], 0);   // classify(c - nb) read dfib[i]
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(dfib[i], fib + lo * 3 * NPTS, sizeof(float) * 3 * NPTS * n, cudaMemcpyHostToDevice, cs);
-        if (e == cudaSuccess) e = cudaEventRecord(ev_in[i], cs);
+            e = cudaMemcpyAsync(dfib[i], fib + lo * 3 * NPTS, sizeof(float) * 3 * NPTS * n, cudaMemcpyHostToDevice, cin);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in[i], cin);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in[i], 0);
+        if (e == cudaSuccess && c >= nb) e = cudaStreamWaitEvent(s, ev_out[i], 0);   // D2H(c - nb) read dlab[i]
         if (e != cudaSuccess) break;
         rc = classify_device(a, dfib[i], (int)n, dlab[i], ddist[i], s, nullptr);
         if (rc) break;
         e = cudaEventRecord(ev_done[i], s);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_done[i], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cout, ev_done[i], 0);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(lab + lo, dlab[i], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, cs);
+            e = cudaMemcpyAsync(lab + lo, dlab[i], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, cout);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(dist + lo, ddist[i], sizeof(float) * n, cudaMemcpyDeviceToHost, cs);
-        if (e == cudaSuccess) e = cudaEventRecord(ev_out[i], cs);
+            e = cudaMemcpyAsync(dist + lo, ddist[i], sizeof(float) * n, cudaMemcpyDeviceToHost, cout);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_out[i], cout);
     }
-    cudaError_t e2 = cudaStreamSynchronize(cs);
+    cudaError_t e2 = cudaStreamSynchronize(cin);
+    if (e == cudaSuccess) e = e2;
+    e2 = cudaStreamSynchronize(cout);
     if (e == cudaSuccess) e = e2;
     // the frees are ordered after the last copies on s
     cudaEvent_t ev_fin = nullptr;
     if (cudaEventCreateWithFlags(&ev_fin, cudaEventDisableTiming) == cudaSuccess) {
-        cudaEventRecord(ev_fin, cs);
+        cudaEventRecord(ev_fin, cout);
         cudaStreamWaitEvent(s, ev_fin, 0);
     }
     for (int i = 0; i < nb; ++i) {
@@ -546,7 +559,8 @@ int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab,
     if (e == cudaSuccess) e = e2;
     if (ev_alloc) cudaEventDestroy(ev_alloc);
     if (ev_fin) cudaEventDestroy(ev_fin);
-    cudaStreamDestroy(cs);
+    cudaStreamDestroy(cin);
+    cudaStreamDestroy(cout);
     if (rc) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "seg_classify: host-buffer pipeline");
     return SEG_OK;
