@@ -55,11 +55,20 @@ def _load():
             lib.oracle_dme_d2.argtypes = [f32p, f32p]
             lib.oracle_dme.restype = ctypes.c_double
             lib.oracle_dme.argtypes = [f32p, f32p]
-            lib.oracle_classify.restype = ctypes.c_int
-            lib.oracle_classify.argtypes = [
-                ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
-                ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
-                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            for fn in (lib.oracle_classify, lib.oracle_classify_paper):
+                fn.restype = ctypes.c_int
+                fn.argtypes = [
+                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                    ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            lib.oracle_polyline_length.restype = ctypes.c_double
+            lib.oracle_polyline_length.argtypes = [f32p]
+            lib.oracle_tn.restype = ctypes.c_double
+            lib.oracle_tn.argtypes = [ctypes.c_double, ctypes.c_double]
+            lib.oracle_endpoint_orientation.restype = ctypes.c_int
+            lib.oracle_endpoint_orientation.argtypes = [f32p, f32p]
+            lib.oracle_paper_score.restype = ctypes.c_double
+            lib.oracle_paper_score.argtypes = [f32p, f32p]
             _lib = lib
     return _lib
 
@@ -90,13 +99,42 @@ def d_me(a, b) -> float:
     return float(_load().oracle_dme(_fp(a), _fp(b)))
 
 
+def polyline_length(a) -> float:
+    """Chord length of a 21-point fiber in mm (reading R16)."""
+    a = _f32(a).reshape(21, 3)
+    return float(_load().oracle_polyline_length(_fp(a)))
+
+
+def tn(ls: float, lc: float) -> float:
+    """Eq. 3 length term."""
+    return float(_load().oracle_tn(float(ls), float(lc)))
+
+
+def endpoint_orientation(a, c) -> int:
+    """1 = inverse, 0 = direct: argmin of the end-point maxima, decided in FP32 (reading R17)."""
+    a, c = _f32(a).reshape(21, 3), _f32(c).reshape(21, 3)
+    return int(_load().oracle_endpoint_orientation(_fp(a), _fp(c)))
+
+
+def paper_score(a, c) -> float:
+    """The complete metric d_ME (inferred orientation) + TN, in mm."""
+    a, c = _f32(a).reshape(21, 3), _f32(c).reshape(21, 3)
+    return float(_load().oracle_paper_score(_fp(a), _fp(c)))
+
+
 def classify(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM,
-             threads: int | None = None, want_d2b: bool = False):
+             threads: int | None = None, want_d2b: bool = False, mode: str = "exact"):
     """Plain-definition classification of fibers [n,21,3] against the atlas.
 
-    Returns dict(label int32[n], dist float64[n], decidable bool[n][, d2b float64[n,B]]).
+    mode "exact": Eq. 2 d_ME (the north_star metric); mode "paper": the paper's complete metric
+    d_ME in the end-point-inferred orientation + TN (Eq. 3), SURVEY.md Sec. 8(f) row f1.
+    Returns dict(label int32[n], dist float64[n], decidable bool[n][, d2b float64[n,B]]);
+    in paper mode d2b holds the per-bundle minimum *score* (mm), not a squared distance.
     """
+    if mode not in ("exact", "paper"):
+        raise ValueError(f"unknown oracle mode {mode!r}")
     lib = _load()
+    fn = lib.oracle_classify if mode == "exact" else lib.oracle_classify_paper
     fib = _f32(fibers).reshape(-1, 21, 3)
     cen = _f32(centroids).reshape(-1, 21, 3)
     bid = np.ascontiguousarray(bundle_id, dtype=np.int32)
@@ -113,7 +151,7 @@ def classify(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM,
     def run(lo, hi):
         if hi <= lo:
             return 0
-        return lib.oracle_classify(
+        return fn(
             fib[lo:].ctypes.data, hi - lo, cen.ctypes.data, bid.ctypes.data, m,
             thr.ctypes.data, b, float(delta),
             label[lo:].ctypes.data, dist[lo:].ctypes.data, dec[lo:].ctypes.data,

@@ -161,3 +161,136 @@ int oracle_classify(const float *fibers, int64_t n,
     free(Db);
     return 0;
 }
+
+/* ======================================================================================
+ * Paper-semantics mode: the paper's final classifier.
+ *
+ *   Eq. 3:  TN = ( |l_S - l_C| / max(l_S, l_C) + 1 )^2 - 1, added to d_ME:
+ *          "the complete distance metric (d_ME + TN)".  Discarding a pair
+ *          before TN when the distance already exceeds the threshold is sound
+ *          because TN >= 0, so it does not change the result and the oracle omits it.
+ *   Lengths: the chord length of the 21-point resampled polyline (reading R16,
+ *          after SPEC.md:124).
+ *   Orientation: the optimised algorithm "uses the distances computed in [the] second
+ *          discarding stage to determine the direction of the fiber" and evaluates the later
+ *          stages in that direction only: orientation = argmin of the two
+ *          end-point maxima, ties -> direct (reading R17, after SPEC.md:251).  That is an
+ *          integer decision taken on floating point, so the oracle takes it in the kernel's
+ *          precision: FP32, each squared distance rounded as fmaf(dz,dz, fmaf(dy,dy, dx*dx))
+ *          on FP32 differences (compiled with -ffp-contract=off, so dx*dx is its own rounding).
+ *   score(a, c) = max_i d_E(a_i, c_o(i)) + TN  in double, o the inferred orientation;
+ *   label(a) = argmin_b { S_b(a) : S_b(a) <= thr_b },  S_b = min_{c in b} score(a, c),
+ *          ties -> lowest bundle id, -1 when none qualifies; dist = S_label.
+ * ====================================================================================== */
+
+/* Chord length of a 21-point polyline, in mm (double). */
+double oracle_polyline_length(const float *a)
+{
+    double l = 0.0;
+    for (int i = 0; i + 1 < NPTS; i++)
+        l += sqrt(oracle_point_d2(a + 3 * i, a + 3 * (i + 1)));
+    return l;
+}
+
+/* Eq. 3. */
+double oracle_tn(double ls, double lc)
+{
+    double mx = ls > lc ? ls : lc;
+    double q = fabs(ls - lc) / mx + 1.0;
+    return q * q - 1.0;
+}
+
+static float f32_point_d2(const float *p, const float *q)
+{
+    float dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
+    return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+/* 1 = inverse, 0 = direct: the argmin of the end-point maxima, decided in FP32. */
+int oracle_endpoint_orientation(const float *a, const float *c)
+{
+    const float *a0 = a, *a20 = a + 3 * (NPTS - 1), *c0 = c, *c20 = c + 3 * (NPTS - 1);
+    float mdir = fmaxf(f32_point_d2(a0, c0), f32_point_d2(a20, c20));
+    float minv = fmaxf(f32_point_d2(a0, c20), f32_point_d2(a20, c0));
+    return minv < mdir ? 1 : 0;
+}
+
+/* The complete metric of one pair in the inferred orientation, in mm. */
+double oracle_paper_score(const float *a, const float *c)
+{
+    int o = oracle_endpoint_orientation(a, c);
+    return sqrt(oracle_max_pointwise_d2(a, c, o)) + oracle_tn(oracle_polyline_length(a), oracle_polyline_length(c));
+}
+
+/*
+ * Classify n fibers by the paper's complete metric (plain definition, every pair, no
+ * discarding).  Arguments and outputs as oracle_classify; dist = the winning score;
+ * sb (nullable) double [n][B] = per-bundle minimum score (+inf for an empty bundle).
+ * The tie band uses the scores (decidable iff no bundle's score lies within delta of its
+ * threshold or of the winner's score).
+ */
+int oracle_classify_paper(const float *fibers, int64_t n,
+                          const float *centroids, const int32_t *bundle_id, int64_t M,
+                          const float *thresh, int32_t B, double delta,
+                          int32_t *label, double *dist, uint8_t *decidable, double *sb)
+{
+    for (int64_t m = 0; m < M; m++)
+        if (bundle_id[m] < 0 || bundle_id[m] >= B)
+            return -1;
+    double *Sb = (double *)malloc(sizeof(double) * (size_t)B);
+    double *lc = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1));
+    if (!Sb || !lc) {
+        free(Sb);
+        free(lc);
+        return -1;
+    }
+    for (int64_t m = 0; m < M; m++)
+        lc[m] = oracle_polyline_length(centroids + (size_t)m * 3 * NPTS);
+    for (int64_t f = 0; f < n; f++) {
+        const float *a = fibers + (size_t)f * 3 * NPTS;
+        for (int32_t b = 0; b < B; b++)
+            Sb[b] = INFINITY;
+        if (!fiber_is_finite(a)) {
+            label[f] = -1;
+            dist[f] = NAN;
+            decidable[f] = 1;
+            if (sb)
+                for (int32_t b = 0; b < B; b++)
+                    sb[(size_t)f * B + b] = NAN;
+            continue;
+        }
+        const double ls = oracle_polyline_length(a);
+        for (int64_t m = 0; m < M; m++) {
+            const float *c = centroids + (size_t)m * 3 * NPTS;
+            int o = oracle_endpoint_orientation(a, c);
+            double s = sqrt(oracle_max_pointwise_d2(a, c, o)) + oracle_tn(ls, lc[m]);
+            if (s < Sb[bundle_id[m]])
+                Sb[bundle_id[m]] = s;
+        }
+        if (sb)
+            for (int32_t b = 0; b < B; b++)
+                sb[(size_t)f * B + b] = Sb[b];
+        int32_t best = -1;
+        for (int32_t b = 0; b < B; b++)
+            if (Sb[b] <= (double)thresh[b] && (best < 0 || Sb[b] < Sb[best]))
+                best = b;
+        label[f] = best;
+        dist[f] = best < 0 ? INFINITY : Sb[best];
+        int32_t bs = -1;
+        for (int32_t b = 0; b < B; b++)
+            if (Sb[b] <= (double)thresh[b] + delta && (bs < 0 || Sb[b] < Sb[bs]))
+                bs = b;
+        int ok = 1;
+        if (bs >= 0) {
+            if (!(Sb[bs] < (double)thresh[bs] - delta))
+                ok = 0;
+            for (int32_t b = 0; b < B && ok; b++)
+                if (b != bs && Sb[b] <= (double)thresh[b] + delta && !(Sb[b] > Sb[bs] + delta))
+                    ok = 0;
+        }
+        decidable[f] = (uint8_t)ok;
+    }
+    free(Sb);
+    free(lc);
+    return 0;
+}
