@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--mode", choices=["exact", "paper"], default="exact",
+                    help="exact: Eq. 2 d_ME (north_star, default); paper: d_ME (inferred orientation) + TN, row f1")
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -50,36 +52,37 @@ def parse():
     return ap.parse_args()
 
 
-def workload_name(cfg):
+def workload_name(cfg, mode="exact"):
     from synth import CONFIGS
     c = CONFIGS[cfg]
     return (f"cfg{cfg}: {c['n_fibers']:,} fibers x {c['n_centroids']:,} centroids "
-            f"({c['n_bundles']} bundles), 21 pts, synthetic")
+            f"({c['n_bundles']} bundles), 21 pts, synthetic"
+            + ("" if mode == "exact" else ", paper-semantics score (d_ME inferred orientation + TN)"))
 
 
 # ------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ------------------------------------------------------------------------------------------
-def time_oracle(cfg, fib, at, target_s):
+def time_oracle(cfg, fib, at, target_s, mode="exact"):
     import oracle
     from synth import sample_indices
     threads = os.cpu_count() or 1
     # calibrate on a small sample, then size the timed sample for ~target_s
     cal = fib[sample_indices(fib.shape[0], max(threads, 8), seed=77)]
     t0 = time.perf_counter()
-    oracle.classify(cal, at.centroids, at.bundle_id, at.thresh, threads=threads)
+    oracle.classify(cal, at.centroids, at.bundle_id, at.thresh, threads=threads, mode=mode)
     dt = max(time.perf_counter() - t0, 1e-3)
     per_fiber = dt / cal.shape[0]
     k = int(max(threads, min(fib.shape[0], target_s / per_fiber)))
     idx = sample_indices(fib.shape[0], k, seed=78)
     sub = fib[idx]
     t0 = time.perf_counter()
-    oracle.classify(sub, at.centroids, at.bundle_id, at.thresh, threads=threads)
+    oracle.classify(sub, at.centroids, at.bundle_id, at.thresh, threads=threads, mode=mode)
     dt = time.perf_counter() - t0
     n = sub.shape[0]
     return dict(value=n * at.M / dt, unit=UNIT, cores=threads, kind="oracle",
                 fibers_per_s=n / dt, seconds=dt,
-                sample=f"{n} seeded fibers (synth.sample_indices seed 78) of {workload_name(cfg)} "
+                sample=f"{n} seeded fibers (synth.sample_indices seed 78) of {workload_name(cfg, mode)} "
                        f"against the full atlas; plain-definition oracle (fp64, no discarding), "
                        f"{threads} host threads over contiguous fiber chunks")
 
@@ -94,14 +97,14 @@ def run_reference(args):
     vals = []
     budget = max(2.0, args.cpu_seconds / max(1, args.steps + args.warmup))
     for i in range(args.warmup + args.steps):
-        r = time_oracle(args.config, fib, at, budget)
+        r = time_oracle(args.config, fib, at, budget, args.mode)
         if i >= args.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
     line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * statistics.median([r["seconds"] for r in vals]),
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=workload_name(args.config), sample=vals[-1]["sample"]),
+                config=dict(workload=workload_name(args.config, args.mode), sample=vals[-1]["sample"]),
                 fibers_per_s=statistics.median([r["fibers_per_s"] for r in vals]),
                 cpu_baseline=dict(value=v, unit=UNIT, cores=vals[-1]["cores"], kind="oracle",
                                   sample=vals[-1]["sample"]),
@@ -193,7 +196,7 @@ def main():
     # atlas: rank 0 generates, NCCL broadcast to the others (setup, untimed)
     at = atlas_for_config(cfg) if rank == 0 else None
     cents, bid, thr = broadcast_atlas(at, spec["n_centroids"], spec["n_bundles"], dev, world)
-    atlas = Atlas(cents, bid, thr)
+    atlas = Atlas(cents, bid, thr, mode=args.mode)
     # this rank's subject (weak scaling: rank r segments subject r of the same shape)
     workers = max(1, (os.cpu_count() or 1) // world)
     t0 = time.perf_counter()
@@ -297,7 +300,7 @@ def main():
     # ---------------- CPU baseline (oracle) on rank 0 at N=1 ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = time_oracle(cfg, fib_np, at, args.cpu_seconds)
+        cpu = time_oracle(cfg, fib_np, at, args.cpu_seconds, args.mode)
         cpu.pop("seconds", None)
 
     if rank == 0:
@@ -305,7 +308,7 @@ def main():
             metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
             ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f32",
             data="synthetic",
-            config=dict(workload=workload_name(cfg), fibers_per_gpu=N, centroids=spec["n_centroids"],
+            config=dict(workload=workload_name(cfg, args.mode), fibers_per_gpu=N, centroids=spec["n_centroids"],
                         bundles=spec["n_bundles"], parallelism=f"fiber-sharded x{world} (one subject per rank)",
                         l2="inputs 1.04 GB > 126 MB L2; no flush needed" if N * 252 > 126e6 else "inputs < L2",
                         generator_s=round(gen_s, 1)),

@@ -73,6 +73,26 @@ typedef struct seg_atlas seg_atlas;
 int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M,
                const float *thresh, int32_t B, int device, seg_atlas **out);
 
+/* Scoring modes of seg_create_ex. */
+enum {
+    SEG_MODE_EXACT = 0,  /* Eq. 2 d_ME, min over both orientations (BASELINE.json north_star) */
+    SEG_MODE_PAPER = 1   /* the paper's final classifier: score =
+                            d_ME in the orientation the end points infer (ties ->
+                            direct) + TN of Eq. 3 on the chord lengths of the
+                            21-point polylines (R16-R18); accept iff score <= thr;
+                            dist = the score */
+};
+
+/*
+ * seg_create_ex -- seg_create with a scoring mode in `flags` (SEG_MODE_EXACT or SEG_MODE_PAPER).
+ * seg_create(...) is seg_create_ex(..., SEG_MODE_EXACT, out).  The cull, the discard cascade and
+ * the closest-bundle rule are shared: every bound of the exact mode is a lower bound of the paper
+ * score too (TN >= 0, and one orientation's maximum >= d_ME), so both modes are exact.
+ * Errors as seg_create, plus SEG_EINVAL for unknown flag bits.
+ */
+int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M,
+                  const float *thresh, int32_t B, int device, uint32_t flags, seg_atlas **out);
+
 /*
  * seg_classify -- label N fibers (Alg. 1 over all fibers).
  *   fibers float32 [N][21][3]; label int32 [N]; dist float32 [N].
@@ -124,6 +144,7 @@ typedef struct {
     int32_t tile_size;    /* 32 */
     int32_t device;       /* CUDA ordinal */
     int64_t device_bytes; /* device memory held by the context */
+    int32_t mode;         /* SEG_MODE_EXACT or SEG_MODE_PAPER */
 } seg_atlas_info;
 
 int seg_get_atlas_info(const seg_atlas *atlas, seg_atlas_info *info);

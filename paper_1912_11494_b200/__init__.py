@@ -43,7 +43,14 @@ def _check_array(x, dtype_np, shape_tail, name):
 class Atlas:
     """An immutable atlas on one CUDA device (seg_create / seg_destroy)."""
 
-    def __init__(self, centroids, bundle_id, thresh, device: int = -1):
+    MODES = {"exact": binding.SEG_MODE_EXACT, "paper": binding.SEG_MODE_PAPER}
+
+    def __init__(self, centroids, bundle_id, thresh, device: int = -1, mode: str = "exact"):
+        """mode "exact": Eq. 2 d_ME (the north_star metric); "paper": the paper's final classifier,
+        d_ME in the end-point-inferred orientation + TN (Eq. 3), see include/seg.h SEG_MODE_PAPER."""
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {sorted(self.MODES)}")
+        self.mode = mode
         _check_array(centroids, np.float32, (21, 3), "centroids")
         _check_array(bundle_id, np.int32, (), "bundle_id")
         _check_array(thresh, np.float32, (), "thresh")
@@ -51,7 +58,7 @@ class Atlas:
             raise ValueError("bundle_id and centroids disagree on M")
         self.M = int(centroids.shape[0])
         self.B = int(thresh.shape[0])
-        self._h = binding.seg_create(centroids, bundle_id, self.M, thresh, self.B, device)
+        self._h = binding.seg_create_ex(centroids, bundle_id, self.M, thresh, self.B, device, self.MODES[mode])
         self.info = binding.seg_get_atlas_info(self._h)
         self.device = self.info["device"]
 

@@ -13,6 +13,7 @@ from . import _build
 
 SEG_OK, SEG_EINVAL, SEG_ENOMEM, SEG_ECUDA = 0, -1, -2, -3
 SEG_NPTS = 21
+SEG_MODE_EXACT, SEG_MODE_PAPER = 0, 1
 SEG_NSTATS = 17
 STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_pass", "lane_test1",
               "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
@@ -29,7 +30,7 @@ class SegError(RuntimeError):
 class seg_atlas_info(ctypes.Structure):
     _fields_ = [("n_centroids", ctypes.c_int64), ("n_bundles", ctypes.c_int32),
                 ("n_tiles", ctypes.c_int32), ("tile_size", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64), ("mode", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -42,6 +43,8 @@ def _load() -> ctypes.CDLL:
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     lib.seg_create.restype = ctypes.c_int
     lib.seg_create.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.seg_create_ex.restype = ctypes.c_int
+    lib.seg_create_ex.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(vp)]
     lib.seg_classify.restype = ctypes.c_int
     lib.seg_classify.argtypes = [vp, vp, i64, vp, vp, vp]
     lib.seg_classify_stats.restype = ctypes.c_int
@@ -64,7 +67,7 @@ def _load() -> ctypes.CDLL:
 
 
 LIB = _load()
-EXPORTS = ("seg_create", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
+EXPORTS = ("seg_create", "seg_create_ex", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
            "seg_profile_enable", "seg_profile_read", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
 
 
@@ -88,6 +91,14 @@ def _ptr(x) -> int | None:
     if hasattr(x, "ctypes"):
         return x.ctypes.data
     raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def seg_create_ex(centroids, bundle_id, M: int, thresh, B: int, device: int = -1, flags: int = SEG_MODE_EXACT) -> int:
+    """seg_create with a scoring mode (SEG_MODE_EXACT / SEG_MODE_PAPER); returns the handle."""
+    out = ctypes.c_void_p()
+    _check(LIB.seg_create_ex(_ptr(centroids), _ptr(bundle_id), int(M), _ptr(thresh), int(B), int(device),
+                             int(flags), ctypes.byref(out)))
+    return out.value
 
 
 def seg_create(centroids, bundle_id, M: int, thresh, B: int, device: int = -1) -> int:

@@ -232,11 +232,7 @@ constexpr int CTAS_PER_SM = 2;
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
 constexpr int STAGES = 3;              // tile ring depth
-#if defined(SEG_FB8)
-constexpr int FB = 8;
-#else
-constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop
-#endif
+constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop (8: register spills)
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
@@ -254,8 +250,8 @@ struct StageMeta {
 };
 
 struct SmemLayout {
-    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, pe = 0, pr = 0, q2e = 0, q2r = 0, best = 0, bars = 0,
-           meta = 0, total = 0;
+    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, pe = 0, pr = 0, q2e = 0, q2r = 0, best = 0, flen = 0,
+           bars = 0, meta = 0, total = 0;
     __host__ __device__ constexpr SmemLayout() {
         size_t o = 0;
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
@@ -265,6 +261,7 @@ struct SmemLayout {
         fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = 1 if the fiber is finite
         fez = o;  o += (size_t)FPC * sizeof(float2);   // (z0, z20)
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
+        flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
         pe = o;   o += (size_t)NCW * 32 * sizeof(uint32_t);
         pr = o;   o += (size_t)NCW * 32 * sizeof(float);
@@ -282,10 +279,6 @@ static_assert(SmemLayout().total <= 233472 / CTAS_PER_SM - 1024, "k_classify sha
 __host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
 
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) {
-#if defined(SEG_SPIN)
-    mbar_wait(bar, parity);
-    return;
-#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAITS_%=:\n\t"
@@ -296,6 +289,22 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) 
 }
 
 __device__ __forceinline__ float key_d2(unsigned long long k) { return __uint_as_float((uint32_t)(k >> 32)); }
+
+// The squared cutoff a fiber's best key implies.  Exact mode keys hold d^2; paper mode keys hold the
+// score s = d_ME + TN (mm) and the cutoff on the squared running max is s^2 rounded UP (TN >= 0, so a
+// pair whose max exceeds s cannot beat s; rounding up keeps that sound).  KEY_NONE reads as NaN,
+// which fminf(thr2, .) ignores.
+template <bool PAPER>
+__device__ __forceinline__ float key_cut2(unsigned long long k) {
+    const float v = key_d2(k);
+    return PAPER ? __fmul_ru(v, v) : v;
+}
+
+// Eq. 3 in FP32 with round-to-nearest ops: ((|ls - lc| / max(ls, lc)) + 1)^2 - 1.
+__device__ __forceinline__ float tn_f32(float ls, float lc) {
+    const float q = __fadd_rn(__fdiv_rn(fabsf(__fsub_rn(ls, lc)), fmaxf(ls, lc)), 1.f);
+    return __fsub_rn(__fmul_rn(q, q), 1.f);
+}
 
 // a2: exact tile lower bound: for every centroid c of the tile,
 // d_ME >= |f10 - c10| >= |f10 - C10| - R10 and d_ME >= min over orientations of the end-point
@@ -324,7 +333,7 @@ __device__ __forceinline__ bool tile_pass_inside(const float4 &E, const float2 &
     return in(d10, r10) && ((in(d00, r0) && in(d2020, r20)) || (in(d020, r20) && in(d200, r0)));
 }
 
-template <bool STATS>
+template <bool STATS, bool PAPER>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemLayout L;
@@ -346,6 +355,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     float4 *fm = fm_all + cw * 32;
     float2 *fez = fez_all + cw * 32;
     unsigned long long *best = best_all + cw * 32;
+    float *flen = reinterpret_cast<float *>(smem + L.flen) + cw * 32;
     uint32_t *pe = reinterpret_cast<uint32_t *>(smem + L.pe) + cw * 32;
     float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * 32;
     uint32_t *q2e = reinterpret_cast<uint32_t *>(smem + L.q2e) + cw * Q2CAP;
@@ -411,6 +421,25 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         fin = __reduce_and_sync(0xffffffffu, fin);   // bit j: every value of fiber j is finite
         __syncwarp();
         fm[lane].w = (((fin >> lane) & 1u) && fjs >= 0) ? 1.f : 0.f;
+        if (PAPER) {
+            // chord length of this lane's fiber (reading R16), FP32, segments summed in order
+            auto pt = [&](int i) -> float4 {
+                if (i == 0) return make_float4(fe[lane].x, fe[lane].z, fez[lane].x, 0.f);
+                if (i == 20) return make_float4(fe[lane].y, fe[lane].w, fez[lane].y, 0.f);
+                if (i == 10) return fm[lane];
+                const float2 a = fxy[mid_slot(i) * 32 + lane];
+                return make_float4(a.x, a.y, fz[mid_slot(i) * 32 + lane], 0.f);
+            };
+            float len = 0.f;
+            float4 prev = pt(0);
+#pragma unroll
+            for (int i = 1; i < NPTS; ++i) {
+                const float4 cur = pt(i);
+                len = __fadd_rn(len, __fsqrt_rn(d2(cur.x, cur.y, cur.z, prev)));
+                prev = cur;
+            }
+            flen[lane] = len;
+        }
         best[lane] = (p.seed && inrange) ? p.seed[fidx] : KEY_NONE;
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
@@ -455,8 +484,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
                 const float thr2 = reinterpret_cast<const TileHdr *>(estage)->thr2;
+                const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
-                const float taul = fminf(thr2, key_d2(best[fl]));
+                const float taul = fminf(thr2, key_cut2<PAPER>(best[fl]));
                 if (r <= taul) {  // re-check against the freshest best (best-first pays here)
                     const float4 *cb = T + c + (o ? 20 * TILE : 0);
                     const int st = o ? -TILE : TILE;
@@ -484,8 +514,16 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         SEG_STEP(6); SEG_STEP(14); SEG_STEP(8); SEG_STEP(12); SEG_STEP(9);
                         SEG_STEP(11);
                         if (STATS) { cnt[ST_PDIST] += 6; cnt[ST_FULL]++; }
-                        // a7: lexicographic (d^2, bundle) minimum
-                        if (r <= thr2) {
+                        // a7: lexicographic (d^2, bundle) minimum; paper mode: (d_ME + TN, bundle)
+                        if (PAPER) {
+                            if (r <= taul) {
+                                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[c].w));
+                                if (sc <= thr) {
+                                    atomicMin(best + fl, ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b);
+                                    if (STATS) cnt[ST_UPD]++;
+                                }
+                            }
+                        } else if (r <= thr2) {
                             atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
                             if (STATS) cnt[ST_UPD]++;
                         }
@@ -524,7 +562,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             const int b = th.bundle;
             long long ts0 = 0;
             if (STATS) ts0 = clock64();
-            const float tau = fminf(thr2, key_d2(best[lane]));
+            const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
             const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sqrtf(tau) + CULL_EPS);
             uint32_t pm = __ballot_sync(0xffffffffu, pass);
@@ -555,37 +593,6 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         jj[q] = pm ? __ffs(pm) - 1 : -1;
                         pm &= pm - 1;
                     }
-#if defined(SEG_T2SKIP)
-                    // test1 first; a fiber no lane passes skips test2 (warp-uniform branch)
-                    float m10q[FB], tjq[FB];
-                    uint32_t any1 = 0;
-#pragma unroll
-                    for (int q = 0; q < FB; ++q) {
-                        const int j = jj[q] < 0 ? 0 : jj[q];
-                        const float4 a10 = fm[j];
-                        tjq[q] = __shfl_sync(0xffffffffu, tau, j);
-                        m10q[q] = d2(a10.x, a10.y, a10.z, c10);
-                        if (jj[q] >= 0 && m10q[q] <= tjq[q]) any1 |= 1u << q;
-                    }
-                    any1 = __reduce_or_sync(0xffffffffu, any1);
-#pragma unroll
-                    for (int q = 0; q < FB; ++q) {
-                        rdv[q] = riv[q] = INFINITY;
-                        tjv[q] = tjq[q];
-                        if ((any1 >> q) & 1u) {
-                            const int j = jj[q];
-                            const float4 E = fe[j];
-                            const float2 Ez = fez[j];
-                            const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)), EZ = f2u(Ez);
-                            const float2 R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);
-                            const float2 R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);
-                            rdv[q] = fmaxf(fmaxf(m10q[q], R0.x), R20.y);
-                            riv[q] = fmaxf(fmaxf(m10q[q], R20.x), R0.y);
-                            if (fminf(rdv[q], riv[q]) <= tjq[q]) hit |= 1u << q;
-                        }
-                        if (STATS && jj[q] >= 0 && m10q[q] <= tjq[q]) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
-                    }
-#else
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         const int j = jj[q] < 0 ? 0 : jj[q];
@@ -600,11 +607,17 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const float2 R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);  // (e0,20, e20,20)
                         rdv[q] = fmaxf(fmaxf(m10, R0.x), R20.y);                        // test2, direct
                         riv[q] = fmaxf(fmaxf(m10, R20.x), R0.y);                        // test2, inverse
+                        if (PAPER) {
+                            // the paper infers the direction from the end points:
+                            // argmin of the end-point maxima, ties -> direct (reading R17); only that
+                            // orientation goes on
+                            if (fmaxf(R20.x, R0.y) < fmaxf(R0.x, R20.y)) rdv[q] = INFINITY;
+                            else riv[q] = INFINITY;
+                        }
                         tjv[q] = tj;
                         if (jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj) hit |= 1u << q;
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
-#endif
                     hit = __reduce_or_sync(0xffffffffu, hit);
 #if defined(SEG_EXP) && SEG_EXP == 3
                     hit = p.n < 0 ? hit : 0;  // experiment: dense test1+test2 only (opaque, so it is not dead code)
@@ -666,7 +679,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                 dd = __int_as_float(0x7fffffff);  // NaN: non-finite fiber
             } else if (key != KEY_NONE) {
                 lab = (int)(uint32_t)(key & 0xffffffffu);
-                dd = __fsqrt_rn(key_d2(key));
+                dd = PAPER ? key_d2(key) : __fsqrt_rn(key_d2(key));   // paper mode keys hold the score
             } else {
                 lab = -1;
                 dd = INFINITY;
@@ -852,15 +865,15 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
         e = cudaEventRecord(after_cull, s);
         if (e != cudaSuccess) return e;
     }
-    if (stats) {
-        e = cudaFuncSetAttribute(k_classify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_classify<true><<<grid, NTHREADS, smem, s>>>(p);
-    } else {
-        e = cudaFuncSetAttribute(k_classify<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_classify<false><<<grid, NTHREADS, smem, s>>>(p);
-    }
+    auto go = [&](auto kern) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) return r;
+        kern<<<grid, NTHREADS, smem, s>>>(p);
+        return cudaSuccess;
+    };
+    if (p.paper) e = stats ? go(k_classify<true, true>) : go(k_classify<false, true>);
+    else e = stats ? go(k_classify<true, false>) : go(k_classify<false, false>);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

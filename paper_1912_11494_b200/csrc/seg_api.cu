@@ -45,7 +45,8 @@ struct seg_atlas {
     int device = 0;
     int64_t M = 0;
     int B = 0, T = 0;
-    float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points
+    int paper = 0;                // SEG_MODE_PAPER: score = d_ME (inferred orientation) + TN
+    float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points (point 0's w = chord length)
     TileHdr *th = nullptr;        // [T]
     BundleHdr *bh = nullptr;      // [B]
     float3 lo{}, inv_cell{};      // Morton grid of the prepass
@@ -309,9 +310,10 @@ static void free_atlas(seg_atlas *a) {
 
 extern "C" void seg_destroy(seg_atlas *a) { free_atlas(a); }
 
-extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M, const float *thresh,
-                          int32_t B, int device, seg_atlas **out) {
+extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M, const float *thresh,
+                             int32_t B, int device, uint32_t flags, seg_atlas **out) {
     if (out) *out = nullptr;
+    if (flags & ~(uint32_t)SEG_MODE_PAPER) return fail(SEG_EINVAL, "seg_create_ex: unknown flags");
     if (!centroids || !bundle_id || !thresh || !out) return fail(SEG_EINVAL, "seg_create: null pointer");
     if (M < 1 || M > INT32_MAX) return fail(SEG_EINVAL, "seg_create: M must be in [1, 2^31-1]");
     if (B < 1) return fail(SEG_EINVAL, "seg_create: B must be >= 1");
@@ -343,6 +345,20 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
 
     // device images
     std::vector<float4> tiles((size_t)P.T * TILE_STRIDE_F4);
+    // chord length of every centroid's 21-point polyline (Eq. 3's l_C, reading R16), in double
+    std::vector<float> clen((size_t)M);
+    for (int64_t m = 0; m < M; ++m) {
+        double l = 0.0;
+        for (int i = 0; i + 1 < NPTS; ++i) {
+            double s2 = 0.0;
+            for (int d = 0; d < 3; ++d) {
+                const double df = (double)cents[(size_t)m * 3 * NPTS + 3 * (i + 1) + d] - (double)cents[(size_t)m * 3 * NPTS + 3 * i + d];
+                s2 += df * df;
+            }
+            l += std::sqrt(s2);
+        }
+        clen[(size_t)m] = (float)l;
+    }
     std::vector<TileHdr> th(P.T);
     std::vector<BundleHdr> bh(B);
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -353,7 +369,7 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
                 tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] =
-                    make_float4(c[0], c[1], c[2], 0.f);
+                    make_float4(c[0], c[1], c[2], i == 0 ? clen[(size_t)m] : 0.f);
                 for (int d = 0; d < 3; ++d) {
                     lo[d] = std::min(lo[d], c[d]);
                     hi[d] = std::max(hi[d], c[d]);
@@ -385,6 +401,7 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
     seg_atlas *a = new (std::nothrow) seg_atlas();
     if (!a) return fail(SEG_ENOMEM, "seg_create: host allocation failed");
     a->device = device;
+    a->paper = (flags & SEG_MODE_PAPER) ? 1 : 0;
     a->M = M;
     a->B = B;
     a->T = P.T;
@@ -428,6 +445,11 @@ extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int6
     return SEG_OK;
 }
 
+extern "C" int seg_create(const float *centroids, const int32_t *bundle_id, int64_t M, const float *thresh,
+                          int32_t B, int device, seg_atlas **out) {
+    return seg_create_ex(centroids, bundle_id, M, thresh, B, device, SEG_MODE_EXACT, out);
+}
+
 extern "C" int seg_get_atlas_info(const seg_atlas *a, seg_atlas_info *info) {
     if (!a || !info) return fail(SEG_EINVAL, "seg_get_atlas_info: null pointer");
     info->n_centroids = a->M;
@@ -436,6 +458,7 @@ extern "C" int seg_get_atlas_info(const seg_atlas *a, seg_atlas_info *info) {
     info->tile_size = TILE;
     info->device = a->device;
     info->device_bytes = a->bytes;
+    info->mode = a->paper ? SEG_MODE_PAPER : SEG_MODE_EXACT;
     return SEG_OK;
 }
 
@@ -466,7 +489,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     uint32_t *tbits = nullptr;
     SEG_CUDA(cudaMallocAsync((void **)&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T), s),
              "seg_classify: cudaMallocAsync");
-    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits};
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits, a->paper};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);

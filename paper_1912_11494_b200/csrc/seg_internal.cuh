@@ -49,6 +49,7 @@ struct ClassifyParams {
     int B, T;
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
     uint32_t *tile_bits;       // [ceil(n / FPC)][T + 1] scratch: k_cull -> k_classify ordered tile lists
+    int paper;                 // 0 = exact Eq. 2 (north_star), 1 = paper semantics (Eq. 3 TN, inferred orientation)
 };
 
 struct MortonParams {
