@@ -136,6 +136,27 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
 int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,
                        int32_t *label, float *dist, uint64_t *stats, void *stream);
 
+/*
+ * seg_group_by_bundle -- row f3: the segmented bundles of a classified subject
+ * (Fig. 1B).  From label[N] (and optionally dist[N]) as seg_classify writes them:
+ *   order   int32 [N]   the fiber indices, STABLY partitioned by bundle: bundle 0's fibers in
+ *                       increasing index, then bundle 1's, ..., then the unassigned ones (label -1,
+ *                       or any label outside [0, B)) last
+ *   offsets int64 [B+2] bundle b occupies order[offsets[b] .. offsets[b+1]); the unassigned ones
+ *                       order[offsets[B] .. offsets[B+1]); offsets[B+1] = N
+ *   dmin, dmax float [B], dsum double [B]  per-bundle min / max / sum of dist (dist >= 0 for every
+ *                       labelled fiber, as seg_classify writes it); +inf / 0 / 0 for an empty
+ *                       bundle.  Requested by a non-NULL dmin (then dmax, dsum and, for N > 0,
+ *                       dist are required); all NULL = no summaries.
+ *                       dsum is accumulated with floating-point atomics: its last bits may vary
+ *                       between runs; order, offsets, dmin and dmax are bitwise deterministic.
+ * All arrays are device memory on one device; ASYNCHRONOUS on `stream`; 1 <= B <= 4095.
+ * Errors: SEG_EINVAL (N < 0 or > 2^31-1, B out of range, null pointer, host memory, mixed devices),
+ * SEG_ECUDA.
+ */
+int seg_group_by_bundle(const int32_t *label, const float *dist, int64_t N, int32_t B, int32_t *order,
+                        int64_t *offsets, float *dmin, float *dmax, double *dsum, void *stream);
+
 /* Shape of a built atlas (for tests and the bench). */
 typedef struct {
     int64_t n_centroids;  /* M */

@@ -14,7 +14,7 @@ import numpy as np
 from . import binding
 from .binding import SegError, STAT_NAMES  # noqa: F401
 
-__all__ = ["Atlas", "SegError", "binding"]
+__all__ = ["Atlas", "SegError", "binding", "group_by_bundle"]
 
 
 def _is_torch(x) -> bool:
@@ -123,3 +123,33 @@ class Atlas:
         stats = np.zeros(binding.SEG_NSTATS, np.uint64)
         binding.seg_classify_stats(self._h, fibers, n, label, dist, stats, self._stream(fibers, stream))
         return label, dist, dict(zip(binding.STAT_NAMES, (int(v) for v in stats)))
+
+
+def group_by_bundle(label, dist, B: int, stream=None):
+    """Row f3: the segmented bundles of a classified subject (seg_group_by_bundle).
+
+    label int32 [N] / dist float32 [N] (torch CUDA tensors, e.g. Atlas.classify's outputs; dist may
+    be None).  Returns (order int32 [N], offsets int64 [B+2], dmin float32 [B], dmax float32 [B],
+    dsum float64 [B]) on the same device: bundle b's fibers are order[offsets[b]:offsets[b+1]] in
+    increasing index, the unassigned ones order[offsets[B]:]; the summaries are None without dist.
+    """
+    import torch
+    if not _is_torch(label) or label.dtype != torch.int32 or not label.is_cuda or label.dim() != 1:
+        raise TypeError("label: expected a 1-D int32 CUDA tensor")
+    if dist is not None and (dist.dtype != torch.float32 or dist.shape != label.shape or dist.device != label.device):
+        raise TypeError("dist: expected a float32 CUDA tensor shaped like label")
+    label = label.contiguous()
+    dist = dist.contiguous() if dist is not None else None
+    n, dev = int(label.shape[0]), label.device
+    order = torch.empty(n, dtype=torch.int32, device=dev)
+    offsets = torch.empty(B + 2, dtype=torch.int64, device=dev)
+    dmin = dmax = dsum = None
+    if dist is not None:
+        dmin = torch.empty(B, dtype=torch.float32, device=dev)
+        dmax = torch.empty(B, dtype=torch.float32, device=dev)
+        dsum = torch.empty(B, dtype=torch.float64, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    binding.seg_group_by_bundle(label, dist if n else None, n, B, order, offsets, dmin, dmax, dsum, stream)
+    return order, offsets, dmin, dmax, dsum
+

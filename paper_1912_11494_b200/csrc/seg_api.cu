@@ -649,6 +649,57 @@ extern "C" int seg_classify_stats(const seg_atlas *a, const float *fibers, int64
     return classify_common(a, fibers, N, label, dist, stream, stats);
 }
 
+// ----------------------------------------------------------------------------------------
+// seg_group_by_bundle (row f3)
+// ----------------------------------------------------------------------------------------
+extern "C" int seg_group_by_bundle(const int32_t *label, const float *dist, int64_t N, int32_t B, int32_t *order,
+                                   int64_t *offsets, float *dmin, float *dmax, double *dsum, void *stream) {
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_group_by_bundle: N must be in [0, 2^31-1]");
+    if (B < 1 || B > group_max_bundles())
+        return fail(SEG_EINVAL, "seg_group_by_bundle: B must be in [1, " + std::to_string(group_max_bundles()) + "]");
+    if (!offsets || (N > 0 && (!label || !order)))
+        return fail(SEG_EINVAL, "seg_group_by_bundle: null pointer");
+    const bool summ = dmin != nullptr;   // summaries requested
+    if (summ && (!dmax || !dsum || (N > 0 && !dist)))
+        return fail(SEG_EINVAL, "seg_group_by_bundle: summaries need dist (N > 0), dmin, dmax and dsum");
+    if (!summ && (dmax || dsum))
+        return fail(SEG_EINVAL, "seg_group_by_bundle: dmax / dsum without dmin");
+    int dev = -1, d2 = -1;
+    const void *ptrs[] = {label, dist, order, offsets, dmin, dmax, dsum};
+    for (const void *q : ptrs) {
+        if (!q) continue;
+        const int k = pointer_kind(q, &d2);
+        if (k < 0) return fail(SEG_ECUDA, "seg_group_by_bundle: no usable CUDA device");
+        if (k != 1) return fail(SEG_EINVAL, "seg_group_by_bundle: all arrays must be device memory");
+        if (dev >= 0 && d2 != dev) return fail(SEG_EINVAL, "seg_group_by_bundle: arrays on different devices");
+        dev = d2;
+    }
+    DeviceGuard guard(dev);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_group_by_bundle: cudaSetDevice failed");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *scratch = nullptr;
+    const size_t words = group_scratch_words(N, B);
+    SEG_CUDA(cudaMallocAsync((void **)&scratch, sizeof(uint32_t) * words, s), "seg_group_by_bundle: cudaMallocAsync");
+    GroupParams gp{};
+    gp.label = label;
+    gp.dist = summ ? dist : nullptr;
+    gp.summ = summ ? 1 : 0;
+    gp.n = N;
+    gp.B = B;
+    gp.hist = scratch;
+    gp.total = scratch + (words - (size_t)(B + 1));
+    gp.offsets = offsets;
+    gp.order = order;
+    gp.gmin = reinterpret_cast<uint32_t *>(dmin);
+    gp.gmax = reinterpret_cast<uint32_t *>(dmax);
+    gp.dsum = dsum;
+    cudaError_t e = launch_group(gp, s);
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "seg_group_by_bundle: launch");
+    g_err.clear();
+    return SEG_OK;
+}
+
 extern "C" int seg_profile_enable(seg_atlas *a, int32_t cap) {
     if (!a || cap < 0) return fail(SEG_EINVAL, "seg_profile_enable: null atlas or negative capacity");
     DeviceGuard guard(a->device);

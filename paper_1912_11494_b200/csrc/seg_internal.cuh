@@ -62,12 +62,31 @@ struct MortonParams {
     int32_t *perm;            // [n]
 };
 
-// Launchers (classify.cu).  All are asynchronous on `s`.
+// Row f3 (group.cu): the stable partition of the fibers by label.
+struct GroupParams {
+    const int32_t *label;      // [n]
+    const float *dist;         // [n] nullable: no summaries
+    int64_t n;
+    int B;
+    int nblk;                  // set by launch_group
+    uint32_t *hist;            // scratch [B+1][nblk]
+    uint32_t *total;           // scratch [B+1]
+    int64_t *offsets;          // [B+2]
+    int32_t *order;            // [n]
+    uint32_t *gmin, *gmax;     // [B] float bits (distances >= 0)
+    double *dsum;              // [B]
+    int summ;                  // summaries requested (gmin / gmax / dsum written, even for n = 0)
+};
+
+// Launchers (classify.cu, group.cu).  All are asynchronous on `s`.
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull = nullptr);
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
 int classify_max_tiles();
 int classify_fibers_per_cta();
+cudaError_t launch_group(GroupParams p, cudaStream_t s);
+size_t group_scratch_words(int64_t n, int B);
+int group_max_bundles();
 
 }  // namespace seg
