@@ -157,6 +157,23 @@ int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,
 int seg_group_by_bundle(const int32_t *label, const float *dist, int64_t N, int32_t B, int32_t *order,
                         int64_t *offsets, float *dmin, float *dmax, double *dsum, void *stream);
 
+/*
+ * seg_resample -- row f2: the step before the path.  Raw streamlines of any
+ * length -> the 21-point fibers seg_classify takes ("resampled using 21 equidistant points",
+ * PAPER.md:93): chord-length parameterisation with linear interpolation (reading R19,
+ * SPEC.md:63-71).  Output point k is the polyline's point at arc length k * L / 20 (L = total chord
+ * length), points 0 and 20 are the input end points exactly; arc lengths and interpolation in double,
+ * each output coordinate rounded to FP32 once.
+ *   points  float32 [P][3]; offsets int64 [N+1]: fiber f = points[offsets[f] .. offsets[f+1])
+ *   out     float32 [N][21][3]
+ * A fiber with fewer than 2 points, zero length (all points coincident) or non-finite points is
+ * invalid input: its 63 outputs are NaN (seg_classify then labels it -1 / NaN).
+ * All arrays device memory on one device; ASYNCHRONOUS on `stream`.  N = 0 is a no-op.
+ * Errors: SEG_EINVAL (N out of range, null pointer with N > 0, host memory, mixed devices,
+ * misalignment: points / out 4 B, offsets 8 B), SEG_ECUDA.
+ */
+int seg_resample(const float *points, const int64_t *offsets, int64_t N, float *out, void *stream);
+
 /* Shape of a built atlas (for tests and the bench). */
 typedef struct {
     int64_t n_centroids;  /* M */

@@ -14,7 +14,7 @@ import numpy as np
 from . import binding
 from .binding import SegError, STAT_NAMES  # noqa: F401
 
-__all__ = ["Atlas", "SegError", "binding", "group_by_bundle"]
+__all__ = ["Atlas", "SegError", "binding", "group_by_bundle", "resample"]
 
 
 def _is_torch(x) -> bool:
@@ -152,4 +152,25 @@ def group_by_bundle(label, dist, B: int, stream=None):
         stream = torch.cuda.current_stream(dev).cuda_stream
     binding.seg_group_by_bundle(label, dist if n else None, n, B, order, offsets, dmin, dmax, dsum, stream)
     return order, offsets, dmin, dmax, dsum
+
+
+def resample(points, offsets, stream=None):
+    """Row f2: raw streamlines -> [N, 21, 3] float32 fibers (seg_resample).
+
+    points float32 [P, 3] and offsets int64 [N + 1] (CSR: fiber f = points[offsets[f]:offsets[f+1]]),
+    torch CUDA tensors on one device.  Invalid fibers (< 2 points, zero length) come out as NaN.
+    """
+    import torch
+    if not (_is_torch(points) and points.is_cuda and points.dtype == torch.float32 and points.dim() == 2
+            and points.shape[1] == 3):
+        raise TypeError("points: expected a float32 CUDA tensor [P, 3]")
+    if not (_is_torch(offsets) and offsets.is_cuda and offsets.dtype == torch.int64 and offsets.dim() == 1):
+        raise TypeError("offsets: expected an int64 CUDA tensor [N + 1]")
+    points, offsets = points.contiguous(), offsets.contiguous()
+    n = int(offsets.shape[0]) - 1
+    out = torch.empty((max(n, 0), 21, 3), dtype=torch.float32, device=points.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(points.device).cuda_stream
+    binding.seg_resample(points, offsets, max(n, 0), out, stream)
+    return out
 

@@ -9,7 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsegb200.so")
-SOURCES = [os.path.join(CSRC, "seg_api.cu"), os.path.join(CSRC, "classify.cu"), os.path.join(CSRC, "group.cu")]
+SOURCES = [os.path.join(CSRC, "seg_api.cu"), os.path.join(CSRC, "classify.cu"), os.path.join(CSRC, "group.cu"),
+           os.path.join(CSRC, "resample.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "seg_internal.cuh"), os.path.join(ROOT, "include", "seg.h")]
 
 NVCC_FLAGS = [

@@ -47,6 +47,8 @@ def _load() -> ctypes.CDLL:
     lib.seg_create_ex.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(vp)]
     lib.seg_group_by_bundle.restype = ctypes.c_int
     lib.seg_group_by_bundle.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp]
+    lib.seg_resample.restype = ctypes.c_int
+    lib.seg_resample.argtypes = [vp, vp, i64, vp, vp]
     lib.seg_classify.restype = ctypes.c_int
     lib.seg_classify.argtypes = [vp, vp, i64, vp, vp, vp]
     lib.seg_classify_stats.restype = ctypes.c_int
@@ -70,7 +72,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTS = ("seg_create", "seg_create_ex", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
-           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
+           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_resample", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
 
 
 def seg_last_error() -> str:
@@ -158,3 +160,7 @@ def seg_group_by_bundle(label, dist, N: int, B: int, order, offsets, dmin=None, 
                         stream: int | None = None) -> None:
     _check(LIB.seg_group_by_bundle(_ptr(label), _ptr(dist), int(N), int(B), _ptr(order), _ptr(offsets),
                                    _ptr(dmin), _ptr(dmax), _ptr(dsum), stream))
+
+
+def seg_resample(points, offsets, N: int, out, stream: int | None = None) -> None:
+    _check(LIB.seg_resample(_ptr(points), _ptr(offsets), int(N), _ptr(out), stream))

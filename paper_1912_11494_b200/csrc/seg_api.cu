@@ -700,6 +700,37 @@ extern "C" int seg_group_by_bundle(const int32_t *label, const float *dist, int6
     return SEG_OK;
 }
 
+// ----------------------------------------------------------------------------------------
+// seg_resample (row f2)
+// ----------------------------------------------------------------------------------------
+extern "C" int seg_resample(const float *points, const int64_t *offsets, int64_t N, float *out, void *stream) {
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_resample: N must be in [0, 2^31-1]");
+    if (N == 0) {
+        g_err.clear();
+        return SEG_OK;
+    }
+    if (!points || !offsets || !out) return fail(SEG_EINVAL, "seg_resample: null pointer with N > 0");
+    if (((uintptr_t)points & 3) || ((uintptr_t)offsets & 7) || ((uintptr_t)out & 3))
+        return fail(SEG_EINVAL, "seg_resample: misaligned pointer");
+    int dev = -1, d2 = -1;
+    const void *ptrs[] = {points, offsets, out};
+    for (const void *q : ptrs) {
+        const int k = pointer_kind(q, &d2);
+        if (k < 0) return fail(SEG_ECUDA, "seg_resample: no usable CUDA device");
+        if (k != 1) return fail(SEG_EINVAL, "seg_resample: all arrays must be device memory");
+        if (dev >= 0 && d2 != dev) return fail(SEG_EINVAL, "seg_resample: arrays on different devices");
+        dev = d2;
+    }
+    DeviceGuard guard(dev);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_resample: cudaSetDevice failed");
+    int sms = 0;
+    SEG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "seg_resample: device attribute");
+    const ResampleParams rp{points, offsets, N, out};
+    SEG_CUDA(launch_resample(rp, sms, (cudaStream_t)stream), "seg_resample: launch");
+    g_err.clear();
+    return SEG_OK;
+}
+
 extern "C" int seg_profile_enable(seg_atlas *a, int32_t cap) {
     if (!a || cap < 0) return fail(SEG_EINVAL, "seg_profile_enable: null atlas or negative capacity");
     DeviceGuard guard(a->device);

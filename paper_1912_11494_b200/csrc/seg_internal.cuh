@@ -78,7 +78,15 @@ struct GroupParams {
     int summ;                  // summaries requested (gmin / gmax / dsum written, even for n = 0)
 };
 
-// Launchers (classify.cu, group.cu).  All are asynchronous on `s`.
+// Row f2 (resample.cu): raw polylines -> 21 points equidistant in chord length.
+struct ResampleParams {
+    const float *points;       // [P][3]
+    const int64_t *offsets;    // [n + 1]: fiber f = points[offsets[f] .. offsets[f + 1])
+    int64_t n;
+    float *out;                // [n][21][3]
+};
+
+// Launchers (classify.cu, group.cu, resample.cu).  All are asynchronous on `s`.
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull = nullptr);
 size_t classify_smem_bytes(int B, int T);
@@ -88,5 +96,6 @@ int classify_fibers_per_cta();
 cudaError_t launch_group(GroupParams p, cudaStream_t s);
 size_t group_scratch_words(int64_t n, int B);
 int group_max_bundles();
+cudaError_t launch_resample(const ResampleParams &p, int sm_count, cudaStream_t s);
 
 }  // namespace seg

@@ -7,7 +7,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_1912_11494_b200 import Atlas, group_by_bundle
+from paper_1912_11494_b200 import Atlas, group_by_bundle, resample
+from synth.raw import raw_streamlines
 from synth import atlas_for_config, fibers_for_config
 
 PEAKS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
@@ -41,3 +42,16 @@ print(json.dumps(dict(row="f3 seg_group_by_bundle", config=f"cfg{cfg} labels of 
                       ms=ms, fibers_per_s=N / (ms * 1e-3), algorithmic_bytes=alg,
                       achieved_gbs=alg / (ms * 1e-3) / 1e9, hbm_peak_gbs=PEAKS["hbm_gbs"],
                       frac=alg / (ms * 1e-3) / 1e9 / PEAKS["hbm_gbs"])))
+
+# row f2: raw streamlines (Catmull-Rom stand-ins, 30-200 points each) of the first 1,000,000 fibers
+NR = min(N, 1_000_000)
+pts, off = raw_streamlines(fibers_for_config(cfg, 0, NR), seed=11)
+P = int(off[-1])
+pts_d, off_d = torch.from_numpy(pts).cuda(), torch.from_numpy(off).cuda()
+ms = timeit(lambda: resample(pts_d, off_d))
+alg = 12 * P + 8 * (NR + 1) + 4 * 63 * NR
+print(json.dumps(dict(row="f2 seg_resample", config=f"cfg{cfg} first {NR:,} fibers as raw streamlines, {P:,} points "
+                      f"(30-200 per fiber, synth/raw.py)", ms=ms, fibers_per_s=NR / (ms * 1e-3),
+                      points_per_s=P / (ms * 1e-3), algorithmic_bytes=alg, achieved_gbs=alg / (ms * 1e-3) / 1e9,
+                      hbm_peak_gbs=PEAKS["hbm_gbs"], frac=alg / (ms * 1e-3) / 1e9 / PEAKS["hbm_gbs"])))
+
