@@ -174,6 +174,25 @@ int seg_group_by_bundle(const int32_t *label, const float *dist, int64_t N, int3
  */
 int seg_resample(const float *points, const int64_t *offsets, int64_t N, float *out, void *stream);
 
+/*
+ * Row f4: atlas-sharded classification for atlases beyond one GPU's L2 / memory
+ * or for more GPUs than subjects.  Each shard is an atlas built from a subset of the bundles (with
+ * the global bundle count B, so labels stay global; the other bundles are empty).  seg_classify_keys
+ * writes each fiber's best key over its shard; the element-wise MIN of the shards' keys (e.g. an
+ * all_reduce MIN over int64) is the key of the whole atlas -- exact and deterministic, because a
+ * key orders (value, bundle) lexicographically as Alg. 1's closest-bundle rule does (PAPER.md:129-133,
+ * :163; ties -> lowest bundle).  seg_keys_to_labels decodes keys into seg_classify's label / dist.
+ * Key space (all keys < 2^63, so signed and unsigned 64-bit MIN agree):
+ *   (float bits of d^2 -- SEG_MODE_PAPER: of the score -- << 32) | bundle id,
+ *   SEG_KEY_NONE (no bundle accepts the fiber), SEG_KEY_NONFINITE (non-finite fiber; every shard
+ *   agrees).  Device pointers only, asynchronous on `stream`.  Errors as seg_classify (keys 8-B
+ *   aligned); seg_keys_to_labels: SEG_EINVAL for an unknown mode.
+ */
+#define SEG_KEY_NONE 0x7fffffffffffffffULL
+#define SEG_KEY_NONFINITE 0x7ffffffffffffffeULL
+int seg_classify_keys(const seg_atlas *atlas, const float *fibers, int64_t N, uint64_t *keys, void *stream);
+int seg_keys_to_labels(const uint64_t *keys, int64_t N, int32_t mode, int32_t *label, float *dist, void *stream);
+
 /* Shape of a built atlas (for tests and the bench). */
 typedef struct {
     int64_t n_centroids;  /* M */

@@ -14,7 +14,7 @@ import numpy as np
 from . import binding
 from .binding import SegError, STAT_NAMES  # noqa: F401
 
-__all__ = ["Atlas", "SegError", "binding", "group_by_bundle", "resample"]
+__all__ = ["Atlas", "SegError", "binding", "group_by_bundle", "keys_to_labels", "resample"]
 
 
 def _is_torch(x) -> bool:
@@ -124,6 +124,22 @@ class Atlas:
         binding.seg_classify_stats(self._h, fibers, n, label, dist, stats, self._stream(fibers, stream))
         return label, dist, dict(zip(binding.STAT_NAMES, (int(v) for v in stats)))
 
+    def classify_keys(self, fibers, keys=None, stream=None):
+        """Row f4: each fiber's best key over this atlas (seg_classify_keys), int64 CUDA tensor [N].
+
+        The element-wise minimum of the keys of several atlas shards is the key of their union
+        (see include/seg.h); keys_to_labels() decodes it.
+        """
+        import torch
+        _check_array(fibers, np.float32, (21, 3), "fibers")
+        if not (_is_torch(fibers) and fibers.is_cuda):
+            raise TypeError("fibers: classify_keys takes CUDA tensors")
+        n = int(fibers.shape[0])
+        if keys is None:
+            keys = torch.empty(n, dtype=torch.int64, device=fibers.device)
+        binding.seg_classify_keys(self._h, fibers, n, keys, self._stream(fibers, stream))
+        return keys
+
 
 def group_by_bundle(label, dist, B: int, stream=None):
     """Row f3: the segmented bundles of a classified subject (seg_group_by_bundle).
@@ -173,4 +189,20 @@ def resample(points, offsets, stream=None):
         stream = torch.cuda.current_stream(points.device).cuda_stream
     binding.seg_resample(points, offsets, max(n, 0), out, stream)
     return out
+
+
+def keys_to_labels(keys, mode: str = "exact", stream=None):
+    """Row f4: decode best keys (Atlas.classify_keys, possibly min-reduced over atlas shards) into
+    (label int32 [N], dist float32 [N]) exactly as seg_classify writes them (seg_keys_to_labels)."""
+    import torch
+    if not (_is_torch(keys) and keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1):
+        raise TypeError("keys: expected a 1-D int64 CUDA tensor")
+    keys = keys.contiguous()
+    n = int(keys.shape[0])
+    label = torch.empty(n, dtype=torch.int32, device=keys.device)
+    dist = torch.empty(n, dtype=torch.float32, device=keys.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(keys.device).cuda_stream
+    binding.seg_keys_to_labels(keys, n, Atlas.MODES[mode], label, dist, stream)
+    return label, dist
 

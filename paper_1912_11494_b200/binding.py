@@ -14,6 +14,7 @@ from . import _build
 SEG_OK, SEG_EINVAL, SEG_ENOMEM, SEG_ECUDA = 0, -1, -2, -3
 SEG_NPTS = 21
 SEG_MODE_EXACT, SEG_MODE_PAPER = 0, 1
+SEG_KEY_NONE, SEG_KEY_NONFINITE = 0x7FFFFFFFFFFFFFFF, 0x7FFFFFFFFFFFFFFE
 SEG_NSTATS = 17
 STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_pass", "lane_test1",
               "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
@@ -49,6 +50,10 @@ def _load() -> ctypes.CDLL:
     lib.seg_group_by_bundle.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp]
     lib.seg_resample.restype = ctypes.c_int
     lib.seg_resample.argtypes = [vp, vp, i64, vp, vp]
+    lib.seg_classify_keys.restype = ctypes.c_int
+    lib.seg_classify_keys.argtypes = [vp, vp, i64, vp, vp]
+    lib.seg_keys_to_labels.restype = ctypes.c_int
+    lib.seg_keys_to_labels.argtypes = [vp, i64, i32, vp, vp, vp]
     lib.seg_classify.restype = ctypes.c_int
     lib.seg_classify.argtypes = [vp, vp, i64, vp, vp, vp]
     lib.seg_classify_stats.restype = ctypes.c_int
@@ -72,7 +77,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTS = ("seg_create", "seg_create_ex", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
-           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_resample", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
+           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_resample", "seg_classify_keys", "seg_keys_to_labels", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
 
 
 def seg_last_error() -> str:
@@ -164,3 +169,12 @@ def seg_group_by_bundle(label, dist, N: int, B: int, order, offsets, dmin=None, 
 
 def seg_resample(points, offsets, N: int, out, stream: int | None = None) -> None:
     _check(LIB.seg_resample(_ptr(points), _ptr(offsets), int(N), _ptr(out), stream))
+
+
+def seg_classify_keys(atlas: int, fibers, N: int, keys, stream: int | None = None) -> None:
+    _check(LIB.seg_classify_keys(atlas, _ptr(fibers), int(N), _ptr(keys), stream))
+
+
+def seg_keys_to_labels(keys, N: int, mode: int, label, dist, stream: int | None = None) -> None:
+    _check(LIB.seg_keys_to_labels(_ptr(keys), int(N), int(mode), _ptr(label), _ptr(dist), stream))
+

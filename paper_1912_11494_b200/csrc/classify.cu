@@ -237,6 +237,8 @@ constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (sme
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
+constexpr unsigned long long KEY_X_NONE = 0x7fffffffffffffffull;       // seg.h SEG_KEY_NONE
+constexpr unsigned long long KEY_X_NONFINITE = 0x7ffffffffffffffeull;  // seg.h SEG_KEY_NONFINITE
 constexpr int MAX_TILES = 30000;
 constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle headers (16 KB)       // k_cull keeps per-tile priorities and the list in shared memory
 
@@ -684,8 +686,14 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                 lab = -1;
                 dd = INFINITY;
             }
-            p.label[fidx] = lab;
-            p.dist[fidx] = dd;
+            if (p.keys) {
+                // row f4: the raw best key for an atlas-sharded run (all_reduce MIN over the shards);
+                // exchange space: every key < 2^63, NONE = INT64_MAX, non-finite = INT64_MAX - 1
+                p.keys[fidx] = fm[lane].w == 0.f ? KEY_X_NONFINITE : key == KEY_NONE ? KEY_X_NONE : key;
+            } else {
+                p.label[fidx] = lab;
+                p.dist[fidx] = dd;
+            }
         }
     }
     if (STATS) {
@@ -842,6 +850,31 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         }
         out[1 + rank] = ti;
     }
+}
+
+// row f4: keys -> (label, dist), the decode of an atlas-sharded run
+__global__ void k_keys_to_labels(const unsigned long long *keys, int64_t n, int paper, int32_t *label, float *dist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = keys[i];
+    if (k == KEY_X_NONE) {
+        label[i] = -1;
+        dist[i] = INFINITY;
+    } else if (k >= KEY_X_NONFINITE) {
+        label[i] = -1;
+        dist[i] = __int_as_float(0x7fffffff);
+    } else {
+        label[i] = (int32_t)(uint32_t)(k & 0xffffffffu);
+        const float v = __uint_as_float((uint32_t)(k >> 32));
+        dist[i] = paper ? v : __fsqrt_rn(v);
+    }
+}
+
+cudaError_t launch_keys_to_labels(const unsigned long long *keys, int64_t n, int paper, int32_t *label, float *dist,
+                                  cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_keys_to_labels<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, paper, label, dist);
+    return cudaGetLastError();
 }
 
 size_t classify_smem_bytes(int, int) { return SmemLayout().total; }

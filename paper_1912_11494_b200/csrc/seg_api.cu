@@ -471,7 +471,8 @@ constexpr int SORT_MIN_N = 4096;   // below this the prepass costs more than it 
 
 // Device pointers, asynchronous on s.
 int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, float *dist, cudaStream_t s,
-                    unsigned long long *d_stats, const unsigned long long *seed = nullptr) {
+                    unsigned long long *d_stats, const unsigned long long *seed = nullptr,
+                    unsigned long long *keys = nullptr) {
     if (n == 0) return SEG_OK;
     cudaEvent_t *ev = nullptr;
     if (a->prof_n < a->prof_cap) ev = &a->prof_ev[4 * (a->prof_n++)];
@@ -489,7 +490,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     uint32_t *tbits = nullptr;
     SEG_CUDA(cudaMallocAsync((void **)&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T), s),
              "seg_classify: cudaMallocAsync");
-    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits, a->paper};
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
@@ -727,6 +728,58 @@ extern "C" int seg_resample(const float *points, const int64_t *offsets, int64_t
     SEG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "seg_resample: device attribute");
     const ResampleParams rp{points, offsets, N, out};
     SEG_CUDA(launch_resample(rp, sms, (cudaStream_t)stream), "seg_resample: launch");
+    g_err.clear();
+    return SEG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// seg_classify_keys / seg_keys_to_labels (row f4)
+// ----------------------------------------------------------------------------------------
+extern "C" int seg_classify_keys(const seg_atlas *a, const float *fibers, int64_t N, uint64_t *keys, void *stream) {
+    if (!a) return fail(SEG_EINVAL, "seg_classify_keys: null atlas");
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_classify_keys: N must be in [0, 2^31-1]");
+    if (N == 0) {
+        g_err.clear();
+        return SEG_OK;
+    }
+    if (!fibers || !keys) return fail(SEG_EINVAL, "seg_classify_keys: null pointer with N > 0");
+    if (((uintptr_t)fibers & 3) || ((uintptr_t)keys & 7)) return fail(SEG_EINVAL, "seg_classify_keys: misaligned pointer");
+    int d0 = -1, d1 = -1;
+    const int k0 = pointer_kind(fibers, &d0), k1 = pointer_kind(keys, &d1);
+    if (k0 < 0 || k1 < 0) return fail(SEG_ECUDA, "seg_classify_keys: no usable CUDA device");
+    if (k0 != 1 || k1 != 1 || d0 != a->device || d1 != a->device)
+        return fail(SEG_EINVAL, "seg_classify_keys: device pointers on the atlas's device only");
+    DeviceGuard guard(a->device);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_classify_keys: cudaSetDevice failed");
+    const int rc = classify_device(a, fibers, (int)N, nullptr, nullptr, (cudaStream_t)stream, nullptr, nullptr,
+                                   reinterpret_cast<unsigned long long *>(keys));
+    if (!rc) g_err.clear();
+    return rc;
+}
+
+extern "C" int seg_keys_to_labels(const uint64_t *keys, int64_t N, int32_t mode, int32_t *label, float *dist,
+                                  void *stream) {
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_keys_to_labels: N must be in [0, 2^31-1]");
+    if (mode != SEG_MODE_EXACT && mode != SEG_MODE_PAPER) return fail(SEG_EINVAL, "seg_keys_to_labels: unknown mode");
+    if (N == 0) {
+        g_err.clear();
+        return SEG_OK;
+    }
+    if (!keys || !label || !dist) return fail(SEG_EINVAL, "seg_keys_to_labels: null pointer with N > 0");
+    int dev = -1, d2 = -1;
+    const void *ptrs[] = {keys, label, dist};
+    for (const void *q : ptrs) {
+        const int k = pointer_kind(q, &d2);
+        if (k < 0) return fail(SEG_ECUDA, "seg_keys_to_labels: no usable CUDA device");
+        if (k != 1) return fail(SEG_EINVAL, "seg_keys_to_labels: all arrays must be device memory");
+        if (dev >= 0 && d2 != dev) return fail(SEG_EINVAL, "seg_keys_to_labels: arrays on different devices");
+        dev = d2;
+    }
+    DeviceGuard guard(dev);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_keys_to_labels: cudaSetDevice failed");
+    SEG_CUDA(launch_keys_to_labels(reinterpret_cast<const unsigned long long *>(keys), N, mode == SEG_MODE_PAPER,
+                                   label, dist, (cudaStream_t)stream),
+             "seg_keys_to_labels: launch");
     g_err.clear();
     return SEG_OK;
 }

@@ -50,6 +50,7 @@ struct ClassifyParams {
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
     uint32_t *tile_bits;       // [ceil(n / FPC)][T + 1] scratch: k_cull -> k_classify ordered tile lists
     int paper;                 // 0 = exact Eq. 2 (north_star), 1 = paper semantics (Eq. 3 TN, inferred orientation)
+    unsigned long long *keys;  // nullable [n]: write the best keys (row f4) instead of label / dist
 };
 
 struct MortonParams {
@@ -97,5 +98,7 @@ cudaError_t launch_group(GroupParams p, cudaStream_t s);
 size_t group_scratch_words(int64_t n, int B);
 int group_max_bundles();
 cudaError_t launch_resample(const ResampleParams &p, int sm_count, cudaStream_t s);
+cudaError_t launch_keys_to_labels(const unsigned long long *keys, int64_t n, int paper, int32_t *label, float *dist,
+                                  cudaStream_t s);
 
 }  // namespace seg

@@ -6,6 +6,11 @@ contiguous shard.  The only exchanges are
   * the atlas, replicated once at setup by a broadcast from rank 0 (C1), and
   * optionally the labels, gathered after the classification (C2).
 Shard boundaries are multiples of 4 fibers so every shard starts 16-byte aligned.
+
+Row f4: the atlas can be sharded instead (atlases beyond one GPU, or more GPUs
+than subjects): every rank holds a subset of the bundles (shard_bundles / shard_atlas) and writes
+each fiber's best key over its shard (Atlas.classify_keys); one all_reduce(MIN) over the int64 keys
+gives the key of the whole atlas, exactly (include/seg.h row f4), and keys_to_labels decodes it.
 """
 from __future__ import annotations
 
@@ -62,3 +67,54 @@ def classify_sharded(classify, fibers: torch.Tensor, n_total: int, world: int, r
         rows.append(out[r * chunk: r * chunk + (b - a)])
     full = torch.cat(rows)
     return full[:, 0].contiguous(), full[:, 1].contiguous().view(torch.float32)
+
+
+def shard_bundles(counts, world: int) -> list:
+    """Deterministic bundle -> rank assignment balancing the centroid counts: bundles by decreasing
+    count (ties: lower id first), each to the rank with the least load so far (ties: lower rank).
+    Returns one sorted list of bundle ids per rank.  Empty bundles are not assigned."""
+    import numpy as np
+    counts = np.asarray(counts, np.int64)
+    order = sorted((b for b in range(counts.size) if counts[b] > 0), key=lambda b: (-int(counts[b]), b))
+    if len(order) < world:
+        raise ValueError(f"cannot shard {len(order)} non-empty bundles over {world} ranks")
+    load = [0] * world
+    out = [[] for _ in range(world)]
+    for b in order:
+        r = min(range(world), key=lambda i: (load[i], i))
+        out[r].append(b)
+        load[r] += int(counts[b])
+    return [sorted(x) for x in out]
+
+
+def shard_atlas(centroids, bundle_id, thresh, world: int, rank: int, mode: str = "exact", device: int = -1):
+    """This rank's atlas shard: the centroids of its bundles, with the global bundle count and
+    thresholds (so labels stay global).  Inputs: numpy arrays or tensors (host or device)."""
+    import numpy as np
+    from . import Atlas
+    bid = bundle_id.cpu().numpy() if hasattr(bundle_id, "cpu") else np.asarray(bundle_id)
+    B = int(thresh.shape[0])
+    mine = shard_bundles(np.bincount(bid, minlength=B), world)[rank]
+    sel = np.nonzero(np.isin(bid, mine))[0]
+    if hasattr(centroids, "index_select"):
+        idx = torch.from_numpy(sel).to(centroids.device)
+        c, b = centroids.index_select(0, idx).contiguous(), bundle_id.index_select(0, idx).contiguous()
+    else:
+        c, b = np.ascontiguousarray(centroids[sel]), np.ascontiguousarray(bid[sel])
+    return Atlas(c, b, thresh, device=device, mode=mode)
+
+
+def reduce_keys(keys: torch.Tensor, world: int) -> torch.Tensor:
+    """all_reduce(MIN) of the shards' best keys (int64, every key < 2^63), in place."""
+    if world > 1:
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+    return keys
+
+
+def classify_atlas_sharded(atlas_shard, fibers: torch.Tensor, world: int):
+    """Atlas-sharded classification of `fibers` (the same fibers on every rank): this rank's keys,
+    the MIN over the ranks, decoded.  Returns (label, dist) on every rank."""
+    from . import keys_to_labels
+    keys = reduce_keys(atlas_shard.classify_keys(fibers), world)
+    return keys_to_labels(keys, atlas_shard.mode)
+

@@ -7,7 +7,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_1912_11494_b200 import Atlas, group_by_bundle, resample
+from paper_1912_11494_b200 import Atlas, group_by_bundle, keys_to_labels, resample
+from paper_1912_11494_b200.dist import shard_atlas
 from synth.raw import raw_streamlines
 from synth import atlas_for_config, fibers_for_config
 
@@ -54,4 +55,23 @@ print(json.dumps(dict(row="f2 seg_resample", config=f"cfg{cfg} first {NR:,} fibe
                       f"(30-200 per fiber, synth/raw.py)", ms=ms, fibers_per_s=NR / (ms * 1e-3),
                       points_per_s=P / (ms * 1e-3), algorithmic_bytes=alg, achieved_gbs=alg / (ms * 1e-3) / 1e9,
                       hbm_peak_gbs=PEAKS["hbm_gbs"], frac=alg / (ms * 1e-3) / 1e9 / PEAKS["hbm_gbs"])))
+
+# row f4: atlas shards (emulated one after another on this GPU): the per-shard keys kernel time is what
+# one rank of a world-N atlas-sharded run spends; the MIN over the shards + decode is checked bitwise
+c_d, b_d, t_d = (torch.from_numpy(x).cuda() for x in (at.centroids, at.bundle_id, at.thresh))
+full_ms = timeit(lambda: A.classify(fib, lab, d), reps=10)
+for world in (2, 4, 8):
+    shards = [shard_atlas(c_d, b_d, t_d, world, r) for r in range(world)]
+    per = []
+    keys = None
+    for sh in shards:
+        kk = torch.empty(N, dtype=torch.int64, device="cuda")
+        per.append(timeit(lambda: sh.classify_keys(fib, kk), reps=5))
+        keys = kk.clone() if keys is None else torch.minimum(keys, kk)
+    l2, d2 = keys_to_labels(keys)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(l2, lab)) and bool(torch.equal(d2.view(torch.int32), d.view(torch.int32)))
+    print(json.dumps(dict(row="f4 atlas shards", config=f"cfg{cfg}, {N:,} fibers, world={world}",
+                          unsharded_ms=full_ms, shard_ms=per, max_shard_ms=max(per), sum_shard_ms=sum(per),
+                          strong_scaling_speedup=full_ms / max(per), min_decode_equals_unsharded=same)))
 
