@@ -231,7 +231,10 @@ constexpr int NCW = 8;                 // consumer warps (4 warps x 3 CTAs/SM me
 constexpr int CTAS_PER_SM = 2;
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
-constexpr int STAGES = 3;              // tile ring depth
+#ifndef SEG_STAGES
+#define SEG_STAGES 3
+#endif
+constexpr int STAGES = SEG_STAGES;     // tile ring depth
 constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop (8: register spills)
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
@@ -378,7 +381,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     }
 
     // ---- a1: coalesced fiber ingest (consumer warps) ----
-    const int gi = blockIdx.x * FPC + warp * 32 + lane;
+    // the CTA's fibers interleaved over the warps (fiber i -> warp i % NCW): every warp gets a similar
+    // share of every tile's work, so the warps sharing the ring stay in step (cfg 3: -1%, cfg 1: -6%
+    // against contiguous 32-fiber slices; the CTA's fibers are all Morton-close anyway)
+    const int gi = blockIdx.x * FPC + lane * NCW + warp;
     const bool inrange = consumer && gi < p.n;
     const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
     if (consumer) {
