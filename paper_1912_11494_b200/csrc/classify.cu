@@ -324,20 +324,6 @@ __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez,
     return p10 && (pdir || pinv);
 }
 
-// tile_may_pass plus a second verdict from the same five distances: are points 0/10/20 of the fiber
-// inside the tile's spheres (in one orientation)?  k_cull orders tiles by it.
-__device__ __forceinline__ bool tile_pass_inside(const float4 &E, const float2 &Ez, const float4 &F10,
-                                                 const TileHdr &h, float s, bool &inside) {
-    const float d10 = d2(F10.x, F10.y, F10.z, h.s10);
-    const float d00 = d2(E.x, E.z, Ez.x, h.s0), d2020 = d2(E.y, E.w, Ez.y, h.s20);
-    const float d020 = d2(E.x, E.z, Ez.x, h.s20), d200 = d2(E.y, E.w, Ez.y, h.s0);
-    auto in = [](float dd, float r) { return dd <= r * r; };
-    const float r0 = h.s0.w + s, r10 = h.s10.w + s, r20 = h.s20.w + s;
-    const float q0 = h.s0.w + CULL_EPS, q10 = h.s10.w + CULL_EPS, q20 = h.s20.w + CULL_EPS;
-    inside = in(d10, q10) && ((in(d00, q0) && in(d2020, q20)) || (in(d020, q20) && in(d200, q0)));
-    return in(d10, r10) && ((in(d00, r0) && in(d2020, r20)) || (in(d020, r20) && in(d200, r0)));
-}
-
 template <bool STATS, bool PAPER>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -727,18 +713,20 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
     uint32_t *tb = sbits, *bb = sbits + twords, *prio = bb + bwords;
     uint16_t *lst = reinterpret_cast<uint16_t *>(prio + p.T);
     __shared__ int nlist;
-    // per bundle the point-10 sphere grown by the bundle threshold: (centre, R); an empty bundle gets a
-    // centre at 1e30 so that no fiber passes it
+    // per bundle the point-10 sphere grown by the bundle threshold: (centre, R^2); an empty bundle (and
+    // the padding up to a multiple of 32) gets a centre at 1e30 so that no fiber passes it
     __shared__ float4 sbs[MAX_SMEM_BUNDLES];
     for (int i = threadIdx.x; i < twords + bwords + p.T; i += FPC) sbits[i] = 0;
     const bool stage_bh = p.B <= MAX_SMEM_BUNDLES;
     auto bsphere = [&](int b) {
+        if (b >= p.B) return make_float4(1e30f, 1e30f, 1e30f, 0.f);
         const BundleHdr h = p.bh[b];
-        return h.t1 > h.t0 ? make_float4(h.s10.x, h.s10.y, h.s10.z, h.s10.w + h.thr + CULL_EPS)
-                           : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+        const float r = h.s10.w + h.thr + CULL_EPS;
+        return h.t1 > h.t0 ? make_float4(h.s10.x, h.s10.y, h.s10.z, r * r) : make_float4(1e30f, 1e30f, 1e30f, 0.f);
     };
+    const int bpad = (p.B + 31) & ~31;
     if (stage_bh)
-        for (int i = threadIdx.x; i < p.B; i += FPC) sbs[i] = bsphere(i);
+        for (int i = threadIdx.x; i < bpad; i += FPC) sbs[i] = bsphere(i);
     const int lane = threadIdx.x & 31;
     const int gi = blockIdx.x * FPC + threadIdx.x;
     bool ok = gi < p.n;
@@ -753,17 +741,15 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         ok = isfinite(E.x) && isfinite(E.y) && isfinite(E.z) && isfinite(E.w) && isfinite(Ez.x) && isfinite(Ez.y) &&
              isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
     }
+    if (!ok) F10 = make_float4(__int_as_float(0x7fffffff), 0.f, 0.f, 0.f);   // NaN: every bound test fails
     __syncthreads();
     // bundles some fiber of the CTA may need (point-10 sphere + threshold, exact)
     for (int b0 = 0; b0 < p.B; b0 += 32) {
         uint32_t m = 0;
 #pragma unroll 8
         for (int j = 0; j < 32; ++j) {
-            const int b = b0 + j;
-            if (b < p.B) {
-                const float4 c = stage_bh ? sbs[b] : bsphere(b);
-                m |= ((ok && d2(F10.x, F10.y, F10.z, c) <= c.w * c.w) ? 1u : 0u) << j;
-            }
+            const float4 c = stage_bh ? sbs[b0 + j] : bsphere(b0 + j);
+            m |= (d2(F10.x, F10.y, F10.z, c) <= c.w ? 1u : 0u) << j;
         }
         m = __reduce_or_sync(0xffffffffu, m);
         if (lane == 0 && m) atomicOr(bb + (b0 >> 5), m);
@@ -775,10 +761,9 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
             const int b = (w << 5) + __ffs(bits) - 1;
             bits &= bits - 1;
             const float4 c = stage_bh ? sbs[b] : bsphere(b);
-            const bool bpass = ok && d2(F10.x, F10.y, F10.z, c) <= c.w * c.w;
+            const bool bpass = d2(F10.x, F10.y, F10.z, c) <= c.w;
             if (!__any_sync(0xffffffffu, bpass)) continue;
             const BundleHdr h = p.bh[b];
-            const float sv = h.thr + CULL_EPS;
             for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
                 // 32 tiles per chunk: independent header loads and tests (ILP)
                 const int nt = min(32, h.t1 - t0);
@@ -786,11 +771,16 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
 #pragma unroll 4
                 for (int j = 0; j < 32; ++j) {
                     if (j < nt) {
-                        const TileHdr th = p.th[t0 + j];
+                        const CullTile ct = p.ct[t0 + j];
+                        // the threshold-only three-sphere bound (squared radii precomputed), and the
                         // processing priority: fibers whose points 0/10/20 lie inside the spheres
-                        bool close;
-                        const bool pass = bpass && tile_pass_inside(E, Ez, F10, th, sv, close);
-                        close = close && pass;
+                        const float d10 = d2(F10.x, F10.y, F10.z, ct.c10);
+                        const float d00 = d2(E.x, E.z, Ez.x, ct.c0), d2020 = d2(E.y, E.w, Ez.y, ct.c20);
+                        const float d020 = d2(E.x, E.z, Ez.x, ct.c20), d200 = d2(E.y, E.w, Ez.y, ct.c0);
+                        const bool pass = bpass && d10 <= ct.c10.w &&
+                                          ((d00 <= ct.c0.w && d2020 <= ct.c20.w) || (d020 <= ct.c20.w && d200 <= ct.c0.w));
+                        const bool close = pass && d10 <= ct.q.y &&
+                                           ((d00 <= ct.q.x && d2020 <= ct.q.z) || (d020 <= ct.q.z && d200 <= ct.q.x));
                         pm |= (pass ? 1u : 0u) << j;
                         cm |= (close ? 1u : 0u) << j;
                     }

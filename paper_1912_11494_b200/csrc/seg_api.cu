@@ -48,6 +48,7 @@ struct seg_atlas {
     int paper = 0;                // SEG_MODE_PAPER: score = d_ME (inferred orientation) + TN
     float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points (point 0's w = chord length)
     TileHdr *th = nullptr;        // [T]
+    CullTile *ct = nullptr;       // [T] squared bounds for k_cull
     BundleHdr *bh = nullptr;      // [B]
     float3 lo{}, inv_cell{};      // Morton grid of the prepass
     int64_t bytes = 0;
@@ -304,6 +305,7 @@ static void free_atlas(seg_atlas *a) {
     free_prof(a);
     cudaFree(a->tiles);
     cudaFree(a->th);
+    cudaFree(a->ct);
     cudaFree(a->bh);
     delete a;
 }
@@ -360,6 +362,13 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
         clen[(size_t)m] = (float)l;
     }
     std::vector<TileHdr> th(P.T);
+    std::vector<CullTile> ct(P.T);
+    auto sq_up = [](double r) {   // r^2 rounded up to FP32
+        const double v = r * r;
+        float f = (float)v;
+        while ((double)f < v) f = std::nextafter(f, INFINITY);
+        return f;
+    };
     std::vector<BundleHdr> bh(B);
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int t = 0; t < P.T; ++t) {
@@ -385,6 +394,14 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
         th[t].thr = thr[b];
         th[t].thr2 = thr[b] * thr[b];
         th[t].pad = 0;
+        {
+            const double sv = (double)thr[b] + (double)CULL_EPS;
+            ct[t].c0 = make_float4(s[0], s[1], s[2], sq_up((double)s[3] + sv));
+            ct[t].c10 = make_float4(s[4], s[5], s[6], sq_up((double)s[7] + sv));
+            ct[t].c20 = make_float4(s[8], s[9], s[10], sq_up((double)s[11] + sv));
+            ct[t].q = make_float4(sq_up((double)s[3] + CULL_EPS), sq_up((double)s[7] + CULL_EPS),
+                                  sq_up((double)s[11] + CULL_EPS), 0.f);
+        }
         std::memcpy(&tiles[(size_t)t * TILE_STRIDE_F4], &th[t], sizeof(TileHdr));
     }
     float maxthr = 0.f;
@@ -418,6 +435,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
                  bbh = bh.size() * sizeof(BundleHdr);
     cudaError_t e = cudaMalloc(&a->tiles, bt);
     if (e == cudaSuccess) e = cudaMalloc(&a->th, bth);
+    if (e == cudaSuccess) e = cudaMalloc(&a->ct, sizeof(CullTile) * ct.size());
     if (e == cudaSuccess) e = cudaMalloc(&a->bh, bbh);
     if (e != cudaSuccess) {
         free_atlas(a);
@@ -427,12 +445,13 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
     }
     e = cudaMemcpy(a->tiles, tiles.data(), bt, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(a->th, th.data(), bth, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(a->ct, ct.data(), sizeof(CullTile) * ct.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(a->bh, bh.data(), bbh, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         free_atlas(a);
         return cuda_fail(e, "seg_create: cudaMemcpy H2D");
     }
-    a->bytes = (int64_t)(bt + bth + bbh);
+    a->bytes = (int64_t)(bt + bth + bbh + sizeof(CullTile) * ct.size());
     // keep stream-ordered scratch cached between seg_classify calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -490,7 +509,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     uint32_t *tbits = nullptr;
     SEG_CUDA(cudaMallocAsync((void **)&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T), s),
              "seg_classify: cudaMallocAsync");
-    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys};
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);

@@ -27,6 +27,15 @@ struct __align__(16) TileHdr {
 };
 static_assert(sizeof(TileHdr) == 64, "TileHdr is 64 B");
 
+// k_cull's copy of a tile's bounds, squared and grown once at seg_create: c0 / c10 / c20 = sphere centre
+// of points 0 / 10 / 20 with w = (radius + thr + CULL_EPS)^2 (the threshold-only bound, rounded up in
+// double so it is never smaller than the exact bound), q = (radius + CULL_EPS)^2 per point (the
+// "inside" priority test; x, y, z = points 0, 10, 20).
+struct __align__(16) CullTile {
+    float4 c0, c10, c20, q;
+};
+static_assert(sizeof(CullTile) == 64, "CullTile is 64 B");
+
 // Per-bundle header: bounding sphere of point 10 over the bundle, tile range [t0, t1).
 struct __align__(16) BundleHdr {
     float4 s10;
@@ -45,6 +54,7 @@ struct ClassifyParams {
     float *dist;              // [n]
     const float4 *tiles;      // [T][TILE_STRIDE_F4]: TileHdr, then [21][32] points
     const TileHdr *th;        // [T]
+    const CullTile *ct;       // [T] k_cull's precomputed squared bounds
     const BundleHdr *bh;      // [B]
     int B, T;
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
