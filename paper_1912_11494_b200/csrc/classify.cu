@@ -1,6 +1,6 @@
 // classify.cu -- sm_100a kernels of the segmentation hot path.
 //
-//   k_morton_hist / k_scan_exclusive / k_morton_scatter   (a9) spatial-order prepass: a counting
+//   k_morton_hist / k_scan_blocks / k_scan_totals / k_morton_scatter   (a9) spatial-order prepass: a counting
 //        sort of the fibers by the Morton code of point 10, so that a warp holds 32 nearby fibers
 //        and its lanes want the same atlas tiles (the B200 analogue of the paper's data-locality
 //        argument).
@@ -148,48 +148,62 @@ __global__ void k_morton_hist(MortonParams p) {
     }
 }
 
-// In-place exclusive scan of MORTON_BUCKETS counters by one CTA of 1024 threads, 4 per thread per
-// round (uint4 loads), carry propagated across rounds.
-__global__ void __launch_bounds__(1024) k_scan_exclusive(uint32_t *hist) {
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry_s;
+// Exclusive scan of the MORTON_BUCKETS counters in two levels: every block of SCAN_B buckets scans its
+// range in place and writes its total (k_scan_blocks, 256 blocks in parallel); one block scans the
+// totals (k_scan_totals); k_morton_scatter adds the block offset of its key.
+constexpr int SCAN_B = 1024;                       // buckets per block: 256 threads x 4
+constexpr int SCAN_NB = MORTON_BUCKETS / SCAN_B;   // 256 blocks
+static_assert(MORTON_BUCKETS % SCAN_B == 0 && SCAN_NB <= 1024, "scan shape");
+
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *warp_sums, uint32_t &total) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) carry_s = 0;
-    __syncthreads();
-    for (int base = 0; base < MORTON_BUCKETS; base += 4096) {
-        uint4 v = reinterpret_cast<uint4 *>(hist + base)[tid];
-        const uint32_t s1 = v.x, s2 = s1 + v.y, s3 = s2 + v.z, s4 = s3 + v.w;
-        uint32_t incl = s4;
+    uint32_t incl = v;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) warp_sums[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = warp_sums[lane], wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
-            }
-            warp_sums[lane] = wi - w;  // exclusive prefix of warp totals
-        }
-        __syncthreads();
-        const uint32_t carry = carry_s;
-        const uint32_t excl = carry + warp_sums[wid] + (incl - s4);
-        reinterpret_cast<uint4 *>(hist + base)[tid] = make_uint4(excl, excl + s1, excl + s2, excl + s3);
-        __syncthreads();
-        if (tid == 1023) carry_s = excl + s4;
-        __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
     }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t w = lane < 8 ? warp_sums[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < 8) warp_sums[lane] = wi - w;
+        if (lane == 7) warp_sums[8] = wi;
+    }
+    __syncthreads();
+    total = warp_sums[8];
+    return warp_sums[wid] + incl - v;
+}
+
+__global__ void __launch_bounds__(256) k_scan_blocks(uint32_t *hist, uint32_t *bsum) {
+    __shared__ uint32_t warp_sums[9];
+    uint4 v = reinterpret_cast<uint4 *>(hist + (size_t)blockIdx.x * SCAN_B)[threadIdx.x];
+    const uint32_t s1 = v.x, s2 = s1 + v.y, s3 = s2 + v.z, s4 = s3 + v.w;
+    uint32_t total;
+    const uint32_t ex = block_excl_scan256(s4, warp_sums, total);
+    reinterpret_cast<uint4 *>(hist + (size_t)blockIdx.x * SCAN_B)[threadIdx.x] = make_uint4(ex, ex + s1, ex + s2, ex + s3);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(256) k_scan_totals(uint32_t *bsum) {
+    __shared__ uint32_t warp_sums[9];
+    const uint32_t v = threadIdx.x < SCAN_NB ? bsum[threadIdx.x] : 0u;
+    uint32_t total;
+    const uint32_t ex = block_excl_scan256(v, warp_sums, total);
+    if (threadIdx.x < SCAN_NB) bsum[threadIdx.x] = ex;
 }
 
 __global__ void k_morton_scatter(MortonParams p) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
-    const uint32_t pos = atomicAdd(p.hist + p.key[i], 1u);
+    const uint32_t k = p.key[i];
+    const uint32_t pos = atomicAdd(p.hist + k, 1u) + __ldg(p.bsum + k / SCAN_B);
     p.perm[pos] = i;
 }
 
@@ -198,10 +212,13 @@ cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int g = (p.n + 255) / 256;
     k_morton_hist<<<(p.n + 256 * MORTON_FPT - 1) / (256 * MORTON_FPT), 256, 0, s>>>(p);
-    k_scan_exclusive<<<1, 1024, 0, s>>>(p.hist);
+    k_scan_blocks<<<SCAN_NB, 256, 0, s>>>(p.hist, p.bsum);
+    k_scan_totals<<<1, 256, 0, s>>>(p.bsum);
     k_morton_scatter<<<g, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
+
+size_t morton_scratch_words() { return (size_t)MORTON_BUCKETS + SCAN_NB; }
 
 // ----------------------------------------------------------------------------------------
 // a1-a8: the classify kernel

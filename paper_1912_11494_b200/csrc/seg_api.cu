@@ -501,9 +501,9 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     if (n >= SORT_MIN_N) {
         SEG_CUDA(cudaMallocAsync((void **)&key, sizeof(uint32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
         SEG_CUDA(cudaMallocAsync((void **)&perm, sizeof(int32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
-        SEG_CUDA(cudaMallocAsync((void **)&hist, sizeof(uint32_t) * MORTON_BUCKETS, s),
+        SEG_CUDA(cudaMallocAsync((void **)&hist, sizeof(uint32_t) * morton_scratch_words(), s),
                  "seg_classify: cudaMallocAsync");
-        MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, perm};
+        MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, hist + MORTON_BUCKETS, perm};
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
     uint32_t *tbits = nullptr;

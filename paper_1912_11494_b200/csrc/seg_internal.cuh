@@ -70,6 +70,7 @@ struct MortonParams {
     float3 inv_cell;          // buckets per mm along each axis
     uint32_t *key;            // [n]
     uint32_t *hist;           // [MORTON_BUCKETS]
+    uint32_t *bsum;           // [MORTON_BUCKETS / 1024] per-block totals, then offsets
     int32_t *perm;            // [n]
 };
 
@@ -99,6 +100,7 @@ struct ResampleParams {
 
 // Launchers (classify.cu, group.cu, resample.cu).  All are asynchronous on `s`.
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
+size_t morton_scratch_words();   // hist + block offsets
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull = nullptr);
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
