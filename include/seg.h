@@ -116,7 +116,7 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
                  int32_t *label, float *dist, void *stream);
 
 /* Number of counters written by seg_classify_stats. */
-#define SEG_NSTATS 17
+#define SEG_NSTATS 22
 /*
  * seg_classify_stats -- seg_classify (device pointers only) with the kernel's
  * per-stage counters (SPEC.md:233-236 CascadeStats, extended), accumulated into the
@@ -130,7 +130,9 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
  *   [10] lane sphere-bound tests (bundle + tile)     [11] CTAs
  *   clock64 cycles summed over consumer warps: [12] tile loop, [13] waiting for a tile,
  *   [14] best-first candidate selection (incl. the candidate rounds it triggers),
- *   [15] candidate rounds, [16] live tile-bound test
+ *   [15] candidate rounds, [16] live tile-bound test, [17] fiber ingest (start -> first barrier)
+ *   [18] candidate rounds run, [19] candidate lanes over those rounds, [20] fibers with a surviving
+ *   orientation after test2 in a tile (best-first selections), [21] of [18]: winners' rounds
  * A separate kernel instantiation; it computes the same labels and distances.
  */
 int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,

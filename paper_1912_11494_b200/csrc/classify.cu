@@ -255,6 +255,7 @@ constexpr int STAGES = SEG_STAGES;     // tile ring depth
 constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop (8: register spills)
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
+constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
 constexpr unsigned long long KEY_X_NONE = 0x7fffffffffffffffull;       // seg.h SEG_KEY_NONE
@@ -264,7 +265,7 @@ constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle h
 
 enum {
     ST_FIBERS = 0, ST_WT_LISTED, ST_WT_COMPUTED, ST_LT_PASS, ST_T1, ST_T2, ST_T34, ST_FULL, ST_UPD,
-    ST_PDIST, ST_SPHERE, ST_CTAS, ST_CYC_CONS, ST_CYC_FULLWAIT, ST_CYC_HIT, ST_CYC_FLUSH, ST_CYC_SPHERE, ST_N
+    ST_PDIST, ST_SPHERE, ST_CTAS, ST_CYC_CONS, ST_CYC_FULLWAIT, ST_CYC_HIT, ST_CYC_FLUSH, ST_CYC_SPHERE, ST_CYC_INGEST, ST_ROUNDS, ST_ROUND_LANES, ST_HITS, ST_ROUND_WIN, ST_N
 };
 
 struct StageMeta {
@@ -285,10 +286,10 @@ struct SmemLayout {
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
         flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
-        pe = o;   o += (size_t)NCW * 32 * sizeof(uint32_t);
-        pr = o;   o += (size_t)NCW * 32 * sizeof(float);
-        q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint32_t);
+        pr = o;   o += (size_t)NCW * PECAP * sizeof(float);
         q2r = o;  o += (size_t)NCW * Q2CAP * sizeof(float);
+        pe = o;   o += (size_t)NCW * PECAP * sizeof(uint16_t);
+        q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint16_t);
         meta = o; o += (size_t)STAGES * sizeof(StageMeta);
         total = (o + 127) & ~(size_t)127;
     }
@@ -364,9 +365,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     float2 *fez = fez_all + cw * 32;
     unsigned long long *best = best_all + cw * 32;
     float *flen = reinterpret_cast<float *>(smem + L.flen) + cw * 32;
-    uint32_t *pe = reinterpret_cast<uint32_t *>(smem + L.pe) + cw * 32;
-    float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * 32;
-    uint32_t *q2e = reinterpret_cast<uint32_t *>(smem + L.q2e) + cw * Q2CAP;
+    uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
+    float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * PECAP;
+    uint16_t *q2e = reinterpret_cast<uint16_t *>(smem + L.q2e) + cw * Q2CAP;
     float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2CAP;
 
     if (threadIdx.x == 0) {
@@ -377,10 +378,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     unsigned long long cnt[ST_N];
+    long long ti0 = 0;
     if (STATS) {
 #pragma unroll
         for (int k = 0; k < ST_N; ++k) cnt[k] = 0;
         cnt[ST_CTAS] = threadIdx.x == 0 ? 1 : 0;
+        ti0 = clock64();
     }
 
     // ---- a1: coalesced fiber ingest (consumer warps) ----
@@ -455,6 +458,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
     __syncthreads();
+    if (STATS && consumer && lane == 0) cnt[ST_CYC_INGEST] += clock64() - ti0;
 
     if (!consumer) {
         // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
@@ -483,12 +487,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         const bool myok = myF10.w != 0.f;
         // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
         // starting from its 3-point running max r
-        auto run_cand = [&](const uint32_t *qe, const float *qr, int n) {
+        auto run_cand = [&](const uint16_t *qe, const float *qr, int n) {
+            if (STATS && lane == 0 && n > 0) { cnt[ST_ROUNDS]++; cnt[ST_ROUND_LANES] += n; if (qe >= pe && qe < pe + PECAP) cnt[ST_ROUND_WIN]++; }
 #if defined(SEG_EXP) && SEG_EXP == 2
             n = 0;  // experiment: no candidate rounds
 #endif
             if (lane < n) {
-                const uint32_t e = qe[lane];
+                const uint32_t e = (uint32_t)qe[lane];
                 float r = qr[lane];
                 const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1, es = (e >> 11) & 3;
                 // the candidate's tile: the ring stage recorded in its entry
@@ -549,7 +554,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             long long tf0 = 0;
             if (STATS) tf0 = clock64();
             __syncwarp();
-            if (np) run_cand(pe, pr, np);
+            for (int w0 = 0; w0 < np; w0 += 32) run_cand(pe + w0, pr + w0, np - w0 >= 32 ? 32 : np - w0);
             np = 0;
             while (n2 > keep) {
                 const int m = n2 >= 32 ? 32 : n2;
@@ -650,9 +655,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const int wl = __ffs(__ballot_sync(0xffffffffu, sb == smin)) - 1;
                         const bool win = lane == wl;
                         const int wo = (ad && rd == sc) ? 0 : 1;
+                        if (STATS && lane == 0) cnt[ST_HITS]++;
                         const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
                         if (win) {
-                            pe[np] = e | ((uint32_t)wo << 10);
+                            pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
                             pr[np] = sc;
                         }
                         ++np;
@@ -660,12 +666,12 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const uint32_t bd = __ballot_sync(0xffffffffu, qd), bi = __ballot_sync(0xffffffffu, qi);
                         if (qd) {
                             const int pos = n2 + __popc(bd & lt_mask);
-                            q2e[pos] = e;
+                            q2e[pos] = (uint16_t)e;
                             q2r[pos] = rd;
                         }
                         if (qi) {
                             const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
-                            q2e[pos] = e | (1u << 10);
+                            q2e[pos] = (uint16_t)(e | (1u << 10));
                             q2r[pos] = ri;
                         }
                         n2 += __popc(bd) + __popc(bi);
