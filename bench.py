@@ -242,7 +242,7 @@ def main():
     value = pairs / (ms_step * 1e-3)
     fibers_per_s = N * world / (ms_step * 1e-3)
     clocks = clk.summary()
-    launches_per_step = 5 if N >= 4096 else 2           # hist, scan, scatter, cull, classify
+    launches_per_step = 6 if N >= 4096 else 2           # hist, scan_blocks, scan_totals, scatter, cull, classify
     res_lab = lab.cpu().numpy()
 
     # ---------------- stage counters + roofline of the dominant kernel ----------------

@@ -1,17 +1,19 @@
 // classify.cu -- sm_100a kernels of the segmentation hot path.
 //
-//   k_morton_hist / k_scan_blocks / k_scan_totals / k_morton_scatter   (a9) spatial-order prepass: a counting
-//        sort of the fibers by the Morton code of point 10, so that a warp holds 32 nearby fibers
-//        and its lanes want the same atlas tiles (the B200 analogue of the paper's data-locality
+//   k_morton_hist / k_scan_blocks / k_scan_totals / k_morton_scatter   (a9) spatial-order prepass:
+//        a counting sort of the fibers by the Morton code of point 10, so that a CTA holds 256 nearby
+//        fibers that want the same atlas tiles (the B200 analogue of the paper's data-locality
 //        argument).
-//   k_classify                                             (a1-a8) one fiber per thread, its 63
-//        coordinates in registers (a1); atlas tiles of 32 centroids streamed into shared memory by
-//        1-D TMA bulk copies through an mbarrier ring fed by a producer warp; per tile an exact
-//        sphere lower bound (a2) decided by warp ballot, then the paper's cascade per centroid:
-//        test1 centre point (a3), test2 end points with sound orientation pruning (a4), test3 four
-//        points (a5), test4 all 21 points with early exit (a6), the
-//        closest-bundle update kept in registers (a7) and a coalesced
-//        epilogue scattered back through the permutation (a8).
+//   k_cull   (a2, list) per CTA of k_classify, the tiles its fibers may need under their bundle
+//        thresholds (bundle point-10 spheres, then the three-sphere tile bound), ordered best-first.
+//   k_classify   (a1-a8) the CTA's fibers in shared memory (cp.async ingest, a1); the listed tiles
+//        streamed into a shared-memory ring by 1-D TMA bulk copies from a producer warp; per tile the
+//        exact sphere bound with each fiber's live cutoff decided by warp ballot (a2), then the
+//        paper's cascade with lane = centroid: test1 centre point (a3), test2 end points in both
+//        orientations (a4), best-first candidate rounds with test3 four points (a5) and test4 the
+//        rest with early exits (a6), the closest-bundle key update (a7,
+//        PAPER.md:129-133, :163) and the epilogue scattered back through the permutation (a8,
+//        PAPER.md:138).  DESIGN.md Sec. 5 has the layout, the roofline and the measurements.
 //
 // FP32 on the CUDA cores: every point distance is the same explicitly-rounded expression
 // (d2 below), so a value reused by an earlier stage is bit-identical to the one the full
@@ -223,26 +225,27 @@ size_t morton_scratch_words() { return (size_t)MORTON_BUCKETS + SCAN_NB; }
 // ----------------------------------------------------------------------------------------
 // a1-a8: the classify kernel
 //
-// CTA = NCW consumer warps (one fiber per consumer lane) + 1 producer warp.
-//   a1  fiber ingest, coalesced: each warp loads its 32 fibers (any order, through the prepass
-//       permutation) with 2 coalesced loads per fiber into shared memory: end points packed for
-//       FFMA2, point 10, and the other 18 points in xy/z planes.
-//   a2  the PRODUCER warp culls: for every bundle and then every tile of a surviving bundle it
-//       tests all FPC fibers of the CTA (4 per lane) against the exact sphere lower bounds with the
-//       fibers' live cutoffs tau = min(thr_b^2, best^2) (read from shared memory, so the cull
-//       tightens as the consumers find matches); a tile some fiber may need is copied into a
-//       STAGES-deep ring by a 1-D TMA bulk copy (cp.async.bulk -> UBLKCP, mbarrier completion),
-//       together with one lane mask per consumer warp.  An end marker closes the stream.
-//   a3+a4  consumers, dense and transposed: lane c holds centroid c's points 0/10/20 (end points
-//       packed), the warp walks the fibers of its mask: test1 (centre point) and test2 (end points,
-//       both orientations, FFMA2) for all 32 centroids at once;
-//   a5+a6  survivors go best-first to candidate rounds (32 candidates per round, every lane busy):
-//       per fiber the centroid with the smallest 3-point score first, then the rest, each re-checked
-//       against the freshest best; test3 = points {3,17,7,13}, test4 = the rest with an early exit
-//       after every group;
-//   a7  a finished orientation updates its fiber's best (d^2, bundle) key with a shared-memory
-//       64-bit atomicMin (lexicographic, so tile order and orientation never matter);
-//   a8  epilogue: label / sqrt(d^2) stored through the permutation.
+// CTA = NCW consumer warps (one fiber per consumer lane; the CTA's 256 Morton-sorted fibers are
+// interleaved over the warps so every warp gets a share of every tile's work) + 1 producer warp.
+//   a1  fiber ingest: every coordinate straight from global memory (through the prepass permutation)
+//       into its shared-memory plane with 4-byte cp.async: end points packed for FFMA2, point 10,
+//       and the other 18 points in xy / z planes; non-finite fibers flagged.
+//   a2  the PRODUCER warp streams the tile list k_cull wrote for this CTA through a STAGES-deep ring
+//       (one 1-D TMA bulk copy per tile, cp.async.bulk -> UBLKCP, mbarrier completion); an end
+//       marker closes the stream.  Each consumer lane re-tests its fiber against the tile's three
+//       spheres with its live cutoff tau = min(thr_b^2, best^2); a warp ballot picks the fibers.
+//   a3+a4  consumers, dense and transposed: lane c holds centroid c's points 0/10/20, the warp walks
+//       its passing fibers 4 at a time: test1 (centre point) and test2 (end points, both
+//       orientations, FFMA2) for all 32 centroids at once;
+//   a5+a6  best-first: per fiber the alive orientation with the smallest 3-point score is its winner
+//       (a winners' round first), every other alive orientation goes to a candidate stack that is
+//       re-checked against the freshest best; test3 = points {3,17,7,13}, test4 = the rest with an
+//       early exit after every group;
+//   a7  a finished orientation updates its fiber's best (d^2, bundle) key -- paper mode:
+//       (d_ME + TN, bundle) -- with a shared-memory 64-bit atomicMin (lexicographic, so tile order
+//       and orientation never matter);
+//   a8  epilogue: label / sqrt(d^2) (paper mode: the score) stored through the permutation, or the
+//       raw key for an atlas-sharded run (row f4).
 // ----------------------------------------------------------------------------------------
 constexpr int NCW = 8;                 // consumer warps (4 warps x 3 CTAs/SM measured slower: 8.74 vs 7.73 ms)
 constexpr int CTAS_PER_SM = 2;
