@@ -130,3 +130,22 @@ def test_tile_bound_is_a_lower_bound_of_dme():
             assert true >= lb - 1e-9
             checked += 1
     assert checked == 360
+
+
+def test_new_entry_points_reject_bad_arguments_without_cuda():
+    """Rows f1-f4 argument checks that fire before any CUDA call."""
+    at = atlas_for_config(0)
+    c, b, t = at.centroids, at.bundle_id, at.thresh
+    out = ctypes.c_void_p(123)
+    L = binding.LIB
+    assert L.seg_create_ex(c.ctypes.data, b.ctypes.data, at.M, t.ctypes.data, at.B, -1, 0x10,
+                           ctypes.byref(out)) == binding.SEG_EINVAL
+    assert "flags" in binding.seg_last_error() and out.value is None
+    assert L.seg_group_by_bundle(None, None, 10, 0, None, None, None, None, None, None) == binding.SEG_EINVAL
+    assert L.seg_group_by_bundle(None, None, 10, 4096, None, None, None, None, None, None) == binding.SEG_EINVAL
+    assert L.seg_group_by_bundle(None, None, -1, 5, None, None, None, None, None, None) == binding.SEG_EINVAL
+    assert L.seg_resample(None, None, -1, None, None) == binding.SEG_EINVAL
+    assert L.seg_resample(None, None, 5, None, None) == binding.SEG_EINVAL
+    assert L.seg_resample(None, None, 0, None, None) == binding.SEG_OK        # N = 0: no-op
+    assert L.seg_keys_to_labels(None, 5, 7, None, None, None) == binding.SEG_EINVAL   # unknown mode
+    assert L.seg_classify_keys(None, None, 5, None, None) == binding.SEG_EINVAL       # null atlas

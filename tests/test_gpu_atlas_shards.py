@@ -33,3 +33,19 @@ def test_sharded_min_equals_unsharded(cfg, n, world, mode):
     assert torch.equal(lab, lab2)
     assert torch.equal(d.view(torch.int32), d2.view(torch.int32))
     assert lab2[3].item() == -1 and torch.isnan(d2[3])
+
+
+def test_keys_argument_errors():
+    from paper_1912_11494_b200 import SegError, binding
+    at = atlas_for_config(0)
+    A = Atlas(torch.from_numpy(at.centroids).cuda(), torch.from_numpy(at.bundle_id).cuda(),
+              torch.from_numpy(at.thresh).cuda())
+    f = torch.zeros((8, 21, 3), dtype=torch.float32, device="cuda")
+    with pytest.raises(SegError):                                   # host keys
+        binding.seg_classify_keys(A.handle, f, 8, np.zeros(8, np.int64), None)
+    with pytest.raises(TypeError):
+        A.classify_keys(f.cpu())
+    k = A.classify_keys(f)                                          # a zero fiber: finite, unassigned
+    lab, d = keys_to_labels(k)
+    torch.cuda.synchronize()
+    assert torch.all(lab == -1) and torch.all(torch.isinf(d))

@@ -115,3 +115,12 @@ def test_paper_constructed_cases():
     lab, d = _gpu(A, np.stack([a, s]).astype(np.float32))
     assert lab[0] == 0 and d[0] == 3.0          # both bundles score 3.0 exactly: lowest id wins
     assert lab[1] == -1 and np.isinf(d[1])
+
+
+def test_paper_host_buffers_equal_device(cfg0p):
+    """The host-buffer pipeline (chunked H2D / classify / D2H) computes the same bits in paper mode."""
+    _, A = cfg0p
+    fib = fibers_for_config(0)
+    lab, d = _gpu(A, fib)
+    hl, hd = A.classify(np.ascontiguousarray(fib))
+    assert np.array_equal(hl, lab) and np.array_equal(hd.view(np.int32), d.view(np.int32))
