@@ -9,3 +9,6 @@ timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo launches_rc=$?
 timeout 1800 ncu --set full --clock-control none --import-source on -k regex:k_classify -s 3 -c 1 -o gpurun_out/prof_classify -f $CMD > gpurun_out/ncu_full.log 2>&1; echo full_rc=$?
 timeout 1800 ncu --set full --clock-control none --import-source on -k regex:k_cull -s 3 -c 1 -o gpurun_out/prof_cull -f $CMD > gpurun_out/ncu_cull.log 2>&1; echo cull_rc=$?
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_torchrun.json 2> gpurun_out/bench_torchrun.err; echo torchrun_rc=$?
+timeout 600 python scripts/bench_rows.py 3 > gpurun_out/bench_rows.jsonl 2> gpurun_out/bench_rows.err; echo rows_rc=$?
+timeout 900 python bench.py --mode paper --steps 20 --warmup 3 --cpu-seconds 5 > gpurun_out/bench_paper.json 2> gpurun_out/bench_paper.err; echo paper_rc=$?
