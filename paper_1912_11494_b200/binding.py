@@ -36,8 +36,14 @@ class seg_atlas_info(ctypes.Structure):
 
 
 def _load() -> ctypes.CDLL:
-    path = _build.LIB
-    if _build.stale():
+    override = os.environ.get("SEG_LIB")   # an alternative build of the same sources (the checked build)
+    if override:
+        if not os.path.exists(override):
+            raise ImportError(f"SEG_LIB={override} does not exist")
+        path = override
+    else:
+        path = _build.LIB
+    if not override and _build.stale():
         _build.build()          # compiles the CUDA library; raises if nvcc is unavailable
     if not os.path.exists(path):
         raise ImportError(f"libsegb200.so missing at {path}; run __graft_entry__.build()")

@@ -205,7 +205,9 @@ __global__ void k_morton_scatter(MortonParams p) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     const uint32_t k = p.key[i];
+    SEG_DCHECK(k < (uint32_t)MORTON_BUCKETS);
     const uint32_t pos = atomicAdd(p.hist + k, 1u) + __ldg(p.bsum + k / SCAN_B);
+    SEG_DCHECK(pos < (uint32_t)p.n);
     p.perm[pos] = i;
 }
 
@@ -396,6 +398,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     const int gi = blockIdx.x * FPC + lane * NCW + warp;
     const bool inrange = consumer && gi < p.n;
     const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
+    SEG_DCHECK(!inrange || (fidx >= 0 && fidx < p.n));
     if (consumer) {
         // every value straight from global into its shared-memory plane with 4-byte cp.async
         // (LDGSTS): this lane copies floats k0 = lane and k1 = 32 + lane (k1 < 63) of each of the
@@ -468,9 +471,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         if (lane == 0) {
             const int32_t *lst_g = reinterpret_cast<const int32_t *>(p.tile_bits) + (size_t)blockIdx.x * (p.T + 1);
             const int nlist = __ldg(lst_g);
+            SEG_DCHECK(nlist >= 0 && nlist <= p.T);
             int k = 0;
             for (; k < nlist; ++k) {
                 const int t = __ldg(lst_g + 1 + k);
+                SEG_DCHECK(t >= 0 && t < p.T);
                 const int s = k % STAGES, u = k / STAGES;
                 if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
                 meta[s].tile = t;
@@ -499,6 +504,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const uint32_t e = (uint32_t)qe[lane];
                 float r = qr[lane];
                 const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1, es = (e >> 11) & 3;
+                SEG_DCHECK(es < STAGES && (e >> 13) == 0);
                 // the candidate's tile: the ring stage recorded in its entry
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
@@ -578,7 +584,6 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             const float4 *stage = ring + s * TILE_STRIDE_F4;
             const TileHdr th = *reinterpret_cast<const TileHdr *>(stage);
             const float thr2 = th.thr2;
-            const int b = th.bundle;
             long long ts0 = 0;
             if (STATS) ts0 = clock64();
             const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
@@ -660,6 +665,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const int wo = (ad && rd == sc) ? 0 : 1;
                         if (STATS && lane == 0) cnt[ST_HITS]++;
                         const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
+                        SEG_DCHECK(np < PECAP && j >= 0 && j < 32);
                         if (win) {
                             pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
                             pr[np] = sc;
@@ -678,6 +684,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                             q2r[pos] = ri;
                         }
                         n2 += __popc(bd) + __popc(bi);
+                        SEG_DCHECK(n2 <= Q2CAP);
                         if (n2 > Q2CAP - 64) flush(31);
                     }
                     if (STATS && lane == 0) cnt[ST_CYC_HIT] += clock64() - th0;
@@ -851,6 +858,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
+        SEG_DCHECK(base <= p.T);
         if (lane == 0) nlist = base;
     }
     __syncthreads();
@@ -870,6 +878,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
             const uint32_t kk = prio[tk];
             rank += (kk > ki || (kk == ki && tk < ti)) ? 1 : 0;
         }
+        SEG_DCHECK(rank < n);
         out[1 + rank] = ti;
     }
 }

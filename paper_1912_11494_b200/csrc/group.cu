@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(GT) kg_scatter(GroupParams p) {
             run[l] = s;
         }
         __syncthreads();
+        SEG_DCHECK(!ok || (int64_t)wcnt[warp * nb + bn] + rank < p.n);
         if (ok) p.order[wcnt[warp * nb + bn] + rank] = (int32_t)i;
         __syncthreads();
     }

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(RT) kr_resample(ResampleParams p) {
                         if (E[mid] >= t) hi = mid; else lo = mid + 1;
                     }
                     const int64_t j = lo;
+                    SEG_DCHECK(j >= 0 && j < nseg);
                     const double s = j > 0 ? E[j - 1] : 0.0;
                     const double ax = P[3 * j], ay = P[3 * j + 1], az = P[3 * j + 2];
                     const double bx = P[3 * (j + 1)], by = P[3 * (j + 1) + 1], bz = P[3 * (j + 1) + 2];
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(RT) kr_resample(ResampleParams p) {
                         const uint32_t segs = __ballot_sync(0xffffffffu, seg);
                         const int owner = reach ? __ffs(reach) - 1 : (last_chunk ? 31 - __clz(segs) : -1);
                         if (owner < 0) break;
+                        SEG_DCHECK(k >= 1 && k < NPTS - 1);
                         if (lane == owner) {
                             const double u = len > 0.0 ? fmin(fmax((t - s) / len, 0.0), 1.0) : 0.0;
                             st[3 * k + 0] = (float)(ax + u * (bx - ax));

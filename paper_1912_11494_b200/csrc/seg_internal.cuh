@@ -6,6 +6,15 @@
 
 namespace seg {
 
+// Checked build (-DSEG_DEBUG, scripts/checked_build.sh): every shared-memory queue index, ring stage,
+// tile index and scatter position is checked on the device and a violation traps (a sticky launch
+// error the host reports).  compute-sanitizer is not available on the GPU pool; this is its stand-in.
+#ifdef SEG_DEBUG
+#define SEG_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SEG_DCHECK(cond) do { } while (0)
+#endif
+
 constexpr int NPTS = 21;                 // points per fiber / centroid
 constexpr int TILE = 32;                 // centroids per tile (one bit per centroid in a u32 mask)
 constexpr int TILE_F4 = NPTS * TILE;     // float4 of tile point data: [21 points][32 centroids]

@@ -149,3 +149,14 @@ def test_new_entry_points_reject_bad_arguments_without_cuda():
     assert L.seg_resample(None, None, 0, None, None) == binding.SEG_OK        # N = 0: no-op
     assert L.seg_keys_to_labels(None, 5, 7, None, None, None) == binding.SEG_EINVAL   # unknown mode
     assert L.seg_classify_keys(None, None, 5, None, None) == binding.SEG_EINVAL       # null atlas
+
+
+def test_seg_lib_override_fails_loudly():
+    """SEG_LIB (the checked build, scripts/checked_build.sh) must name an existing library: a missing
+    one is an ImportError, never a silent fallback to another build or to the CPU."""
+    import subprocess, sys
+    env = dict(os.environ, SEG_LIB="/nonexistent/libsegb200.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_1912_11494_b200.binding"], env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "SEG_LIB" in r.stderr
