@@ -257,7 +257,10 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 #define SEG_STAGES 3
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
-constexpr int FB = 4;                  // fibers per step of the dense test1+test2 loop (8: register spills)
+#ifndef SEG_FB
+#define SEG_FB 4
+#endif
+constexpr int FB = SEG_FB;             // fibers per step of the dense test1+test2 loop (cfg 3: 3 -> +1%, 5 -> +3%, 8 -> +16%)
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
@@ -495,7 +498,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         const bool myok = myF10.w != 0.f;
         // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
         // starting from its 3-point running max r
-        auto run_cand = [&](const uint16_t *qe, const float *qr, int n) {
+        // excl: the round's entries are distinct fibers (a winners' round: at most one winner per
+        // fiber per tile), so the best key is updated by a plain compare-and-store, not an atomic
+        auto run_cand = [&](const uint16_t *qe, const float *qr, int n, bool excl) {
             if (STATS && lane == 0 && n > 0) { cnt[ST_ROUNDS]++; cnt[ST_ROUND_LANES] += n; if (qe >= pe && qe < pe + PECAP) cnt[ST_ROUND_WIN]++; }
 #if defined(SEG_EXP) && SEG_EXP == 2
             n = 0;  // experiment: no candidate rounds
@@ -544,12 +549,16 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                             if (r <= taul) {
                                 const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[c].w));
                                 if (sc <= thr) {
-                                    atomicMin(best + fl, ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b);
+                                    const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b;
+                                    if (excl) { if (kk < best[fl]) best[fl] = kk; } else
+                                    atomicMin(best + fl, kk);
                                     if (STATS) cnt[ST_UPD]++;
                                 }
                             }
                         } else if (r <= thr2) {
-                            atomicMin(best + fl, ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b);
+                            const unsigned long long kk = ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b;
+                            if (excl) { if (kk < best[fl]) best[fl] = kk; } else
+                            atomicMin(best + fl, kk);
                             if (STATS) cnt[ST_UPD]++;
                         }
                     }
@@ -563,12 +572,13 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             long long tf0 = 0;
             if (STATS) tf0 = clock64();
             __syncwarp();
-            for (int w0 = 0; w0 < np; w0 += 32) run_cand(pe + w0, pr + w0, np - w0 >= 32 ? 32 : np - w0);
+            SEG_DCHECK(np <= 32);
+            if (np > 0) run_cand(pe, pr, np, true);
             np = 0;
             while (n2 > keep) {
                 const int m = n2 >= 32 ? 32 : n2;
                 n2 -= m;
-                run_cand(q2e + n2, q2r + n2, m);
+                run_cand(q2e + n2, q2r + n2, m, false);
             }
             if (STATS && lane == 0) cnt[ST_CYC_FLUSH] += clock64() - tf0;
         };
@@ -649,18 +659,23 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                     if (!hit) continue;
                     long long th0 = 0;
                     if (STATS) th0 = clock64();
+                    // one copy of the selection code, the step's hit fibers picked by selects
+                    // (keeps the kernel's code small: the q loop unrolled it FB times, flush included)
+                    for (uint32_t hb = hit; hb; hb &= hb - 1) {
+                        const int q = __ffs(hb) - 1;
+                        int j = jj[0];
+                        float rd = rdv[0], ri = riv[0], tj = tjv[0];
 #pragma unroll
-                    for (int q = 0; q < FB; ++q) {
-                        if (!((hit >> q) & 1u)) continue;
-                        const int j = jj[q];
-                        const float rd = rdv[q], ri = riv[q], tj = tjv[q];
+                        for (int t = 1; t < FB; ++t)
+                            if (q == t) { j = jj[t]; rd = rdv[t]; ri = riv[t]; tj = tjv[t]; }
                         const bool ad = rd <= tj, ai = ri <= tj;
                         // best-first: the centroid with the smallest 3-point score goes to the
                         // winners' round, every other surviving orientation to q2
                         const float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
-                        const uint32_t sb = __float_as_uint(sc);
-                        const uint32_t smin = __reduce_min_sync(0xffffffffu, sb);
-                        const int wl = __ffs(__ballot_sync(0xffffffffu, sb == smin)) - 1;
+                        // the lane rides in the score's 5 low mantissa bits: REDUX.MIN names the winner
+                        // directly (a heuristic choice; every survivor is still evaluated)
+                        const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
+                        const int wl = (int)(smin & 31u);
                         const bool win = lane == wl;
                         const int wo = (ad && rd == sc) ? 0 : 1;
                         if (STATS && lane == 0) cnt[ST_HITS]++;
