@@ -226,3 +226,42 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def seed_eval(cfg=3, n=2000, reps=1):
+    """Quality of a cheap seed: the fiber's nearest tile by sphere centres (max of the point-10 and the
+    better-orientation end-point centre distances), then the exact d_ME against that tile's
+    representative member (the member nearest its sphere centres)."""
+    at = atlas_for_config(cfg)
+    full = fibers_for_config(cfg, 0, 200000)
+    fib = full[sample_indices(len(full), n, seed=5)].astype(np.float64)
+    r = oracle.classify(fib.astype(np.float32), at.centroids, at.bundle_id, at.thresh)
+    lab, dfin = r["label"], np.where(r["label"] >= 0, r["dist"], np.inf)
+    tb, mem, sph = current_plan(at)
+    S = sph.astype(np.float64)
+    C = at.centroids.astype(np.float64)
+    fl = canon_flips(at)
+    Cc, _ = feats(at, fl)
+    # representative of each tile: member minimising the max distance to the three sphere centres
+    rep = np.zeros(len(tb), int)
+    for t in range(len(tb)):
+        m = np.unique(mem[t])
+        d = np.max([np.sqrt(((Cc[m, p] - S[t, q, :3]) ** 2).sum(1)) for q, p in enumerate((0, 10, 20))], axis=0)
+        rep[t] = m[np.argmin(d)]
+    f0, f10, f20 = fib[:, 0], fib[:, 10], fib[:, 20]
+    dc = lambda P, q: np.sqrt(((P[:, None] - S[None, :, q, :3]) ** 2).sum(-1))
+    prox = np.maximum(dc(f10, 1), np.minimum(np.maximum(dc(f0, 0), dc(f20, 2)), np.maximum(dc(f20, 0), dc(f0, 2))))
+    order = np.argsort(prox, axis=1)[:, :reps]
+    thr = at.thresh.astype(np.float64)
+    dseed = np.full(n, np.inf)
+    for k in range(reps):
+        t = order[:, k]
+        c = C[rep[t]]
+        dd = np.minimum(np.sqrt(((fib - c) ** 2).sum(-1)).max(1), np.sqrt(((fib - c[:, ::-1]) ** 2).sum(-1)).max(1))
+        ok = dd <= thr[tb[t]]
+        dseed = np.where(ok, np.minimum(dseed, dd), dseed)
+    lbl = np.isfinite(dfin)
+    print(f"reps={reps}: labelled {lbl.mean():.3f}; seeded {np.isfinite(dseed).mean():.3f} "
+          f"(of labelled {np.isfinite(dseed[lbl]).mean():.3f}); seed == final {np.mean(dseed[lbl] <= dfin[lbl] * (1 + 1e-6)):.3f}; "
+          f"median d_seed/d_final {np.median(dseed[lbl & np.isfinite(dseed)] / dfin[lbl & np.isfinite(dseed)]):.3f}")
+    return dseed, dfin
