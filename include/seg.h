@@ -106,6 +106,8 @@ int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M,
  *   Output is bitwise deterministic: independent of N, of the chunking, of the
  *   stream, of the GPU count and of the order of centroids in seg_create.
  *   Scratch is stream-ordered (cudaMallocAsync).  fibers needs 4-byte alignment.
+ *   Device-resident inputs run in slices of at most 2^23 fibers (bounded scratch: 8 B per fiber
+ *   plus 2 (T + 2) B per 256 fibers); fibers are independent, so the slicing changes no result.
  *   N = 0 is a no-op returning SEG_OK.
  * Errors: SEG_EINVAL (null atlas, null pointer with N > 0, N > 2^31 - 1, mixed host
  * and device pointers, a device pointer on another device, misalignment),
@@ -226,7 +228,8 @@ int seg_plan_tiles(const float *centroids, const int32_t *bundle_id, int64_t M, 
 /*
  * Profiling hook (bench.py only; NOT thread-safe, unlike the rest of the context):
  * after seg_profile_enable(atlas, cap) the first `cap` device-pointer seg_classify calls
- * on `atlas` record CUDA events on their stream before the spatial prepass, before the
+ * on `atlas` (one record per slice of at most 2^23 fibers, see seg_classify) record CUDA
+ * events on their stream before the spatial prepass, before the
  * tile-list kernel (k_cull), before the classify kernel and after it.  seg_profile_read
  * synchronises on those events and writes, per recorded call i < min(count, capacity),
  * prepass_ms[i], cull_ms[i] and classify_ms[i] (nullable host arrays);

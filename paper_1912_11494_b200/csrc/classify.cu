@@ -269,6 +269,9 @@ constexpr unsigned long long KEY_NONE = ~0ull;
 constexpr unsigned long long KEY_X_NONE = 0x7fffffffffffffffull;       // seg.h SEG_KEY_NONE
 constexpr unsigned long long KEY_X_NONFINITE = 0x7ffffffffffffffeull;  // seg.h SEG_KEY_NONFINITE
 constexpr int MAX_TILES = 30000;
+static_assert(MAX_TILES < 65535, "k_cull's per-CTA tile lists hold u16 tile indices");
+// per CTA of k_cull / k_classify: [count, tiles...] as u16, padded to a whole 32-bit word
+__host__ __device__ constexpr int cull_stride(int T) { return (T + 2) & ~1; }
 constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle headers (16 KB)       // k_cull keeps per-tile priorities and the list in shared memory
 
 enum {
@@ -472,7 +475,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     if (!consumer) {
         // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
         if (lane == 0) {
-            const int32_t *lst_g = reinterpret_cast<const int32_t *>(p.tile_bits) + (size_t)blockIdx.x * (p.T + 1);
+            const unsigned short *lst_g =
+                reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)blockIdx.x * cull_stride(p.T);
             const int nlist = __ldg(lst_g);
             SEG_DCHECK(nlist >= 0 && nlist <= p.T);
             int k = 0;
@@ -882,8 +886,8 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
     // gives the same result (the (d^2, bundle) minimum is order-independent); a good order makes
     // the running best tight early, which prunes the later tiles.
     const int n = nlist;
-    int32_t *out = reinterpret_cast<int32_t *>(p.tile_bits) + (size_t)blockIdx.x * (p.T + 1);
-    if (threadIdx.x == 0) out[0] = n;
+    uint16_t *out = reinterpret_cast<uint16_t *>(p.tile_bits) + (size_t)blockIdx.x * cull_stride(p.T);
+    if (threadIdx.x == 0) out[0] = (uint16_t)n;
     for (int i = threadIdx.x; i < n; i += FPC) {
         const int ti = lst[i];
         const uint32_t ki = prio[ti];
@@ -894,7 +898,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
             rank += (kk > ki || (kk == ki && tk < ti)) ? 1 : 0;
         }
         SEG_DCHECK(rank < n);
-        out[1 + rank] = ti;
+        out[1 + rank] = (uint16_t)ti;
     }
 }
 
@@ -929,7 +933,7 @@ int classify_fibers_per_cta() { return FPC; }
 
 int classify_max_tiles() { return MAX_TILES; }
 
-size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(T + 1); }
+size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(cull_stride(T) / 2); }
 
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull) {
     if (p.n <= 0) return cudaSuccess;

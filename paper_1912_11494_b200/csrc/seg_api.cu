@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -523,6 +524,29 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     return SEG_OK;
 }
 
+// Device inputs are classified in slices of at most DEV_CHUNK fibers.  Fibers are independent, so the
+// result does not depend on the slicing; it bounds the per-call scratch (Morton keys and permutation,
+// 8 B per fiber; the per-CTA tile lists, (T + 2) x 2 B per 256 fibers) whatever N is.  Configurations
+// up to 8.4 M fibers run as one slice.
+constexpr int64_t DEV_CHUNK = int64_t(1) << 23;
+int classify_device_sliced(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab, float *dist,
+                           cudaStream_t s, unsigned long long *d_stats, const unsigned long long *seed = nullptr,
+                           unsigned long long *keys = nullptr) {
+    // SEG_DEV_CHUNK (tests only): a smaller slice, to exercise the slicing at small N
+    static const int64_t chunk = [] {
+        const char *e = std::getenv("SEG_DEV_CHUNK");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? std::min<int64_t>(v, DEV_CHUNK) : DEV_CHUNK;
+    }();
+    for (int64_t c0 = 0; c0 < N; c0 += chunk) {
+        const int n = (int)std::min<int64_t>(chunk, N - c0);
+        const int rc = classify_device(a, fib + c0 * 3 * NPTS, n, lab ? lab + c0 : nullptr, dist ? dist + c0 : nullptr,
+                                       s, d_stats, seed ? seed + c0 : nullptr, keys ? keys + c0 : nullptr);
+        if (rc) return rc;
+    }
+    return SEG_OK;
+}
+
 // Host pointers: chunked H2D -> classify -> D2H over three streams (copy-in, the caller's stream
 // for the kernels, copy-out) and NB device buffer sets, so that the host->device copy of chunk c+1
 // runs while chunk c is classified and chunk c-1 is copied back.  Buffer set i is reused by chunk
@@ -642,8 +666,8 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
         SEG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * SEG_NSTATS, s),
                  "seg_classify_stats: memset");
     }
-    int rc = classify_device(a, fibers, (int)N, label, dist, s, d_stats,
-                             reinterpret_cast<const unsigned long long *>(seed));
+    int rc = classify_device_sliced(a, fibers, N, label, dist, s, d_stats,
+                                    reinterpret_cast<const unsigned long long *>(seed));
     if (stats) {
         unsigned long long h[SEG_NSTATS];
         cudaError_t e = cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -770,8 +794,8 @@ extern "C" int seg_classify_keys(const seg_atlas *a, const float *fibers, int64_
         return fail(SEG_EINVAL, "seg_classify_keys: device pointers on the atlas's device only");
     DeviceGuard guard(a->device);
     if (!guard.ok) return fail(SEG_ECUDA, "seg_classify_keys: cudaSetDevice failed");
-    const int rc = classify_device(a, fibers, (int)N, nullptr, nullptr, (cudaStream_t)stream, nullptr, nullptr,
-                                   reinterpret_cast<unsigned long long *>(keys));
+    const int rc = classify_device_sliced(a, fibers, N, nullptr, nullptr, (cudaStream_t)stream, nullptr, nullptr,
+                                          reinterpret_cast<unsigned long long *>(keys));
     if (!rc) g_err.clear();
     return rc;
 }

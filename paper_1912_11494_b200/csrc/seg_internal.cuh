@@ -67,7 +67,7 @@ struct ClassifyParams {
     const BundleHdr *bh;      // [B]
     int B, T;
     unsigned long long *stats; // [SEG_NSTATS] (stats instantiation only)
-    uint32_t *tile_bits;       // [ceil(n / FPC)][T + 1] scratch: k_cull -> k_classify ordered tile lists
+    uint32_t *tile_bits;       // scratch: per CTA of FPC fibers, [count, tiles...] as u16 (cull_stride(T)): k_cull -> k_classify
     int paper;                 // 0 = exact Eq. 2 (north_star), 1 = paper semantics (Eq. 3 TN, inferred orientation)
     unsigned long long *keys;  // nullable [n]: write the best keys (row f4) instead of label / dist
 };
