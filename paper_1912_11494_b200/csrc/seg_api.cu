@@ -53,6 +53,9 @@ struct seg_atlas {
     BundleHdr *bh = nullptr;      // [B]
     float3 lo{}, inv_cell{};      // Morton grid of the prepass
     int64_t bytes = 0;
+    // the atlas's own stream-ordered memory pool for per-call scratch, kept cached between calls (release
+    // threshold: never); nullptr -> the device's default pool, left as the caller configured it
+    cudaMemPool_t pool = nullptr;
     // profiling hook (seg_profile_enable / seg_profile_read); mutable, not thread-safe
     mutable std::vector<cudaEvent_t> prof_ev;  // 4 per recorded call
     mutable int prof_cap = 0, prof_n = 0;
@@ -308,6 +311,8 @@ static void free_atlas(seg_atlas *a) {
     cudaFree(a->th);
     cudaFree(a->ct);
     cudaFree(a->bh);
+    // outstanding stream-ordered frees are completed by the driver before the pool goes away
+    if (a->pool) cudaMemPoolDestroy(a->pool);
     delete a;
 }
 
@@ -453,11 +458,19 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
         return cuda_fail(e, "seg_create: cudaMemcpy H2D");
     }
     a->bytes = (int64_t)(bt + bth + bbh + sizeof(CullTile) * ct.size());
-    // keep stream-ordered scratch cached between seg_classify calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr_bytes = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr_bytes);
+    // a private pool keeps the per-call scratch cached between seg_classify calls without changing the
+    // device's default pool; if one cannot be created the default pool is used as it is
+    {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        if (cudaMemPoolCreate(&a->pool, &props) == cudaSuccess) {
+            uint64_t thr_bytes = UINT64_MAX;
+            cudaMemPoolSetAttribute(a->pool, cudaMemPoolAttrReleaseThreshold, &thr_bytes);
+        } else {
+            a->pool = nullptr;
+        }
     }
     cudaGetLastError();
     *out = a;
@@ -489,6 +502,31 @@ namespace {
 
 constexpr int SORT_MIN_N = 4096;   // below this the prepass costs more than it saves
 
+// Stream-ordered scratch from the atlas's pool; everything obtained is released (stream-ordered) when the
+// holder goes out of scope, on every return path.
+struct Scratch {
+    cudaStream_t s;
+    cudaMemPool_t pool;
+    void *ptrs[8] = {};
+    int n = 0;
+    Scratch(cudaStream_t s_, cudaMemPool_t pool_) : s(s_), pool(pool_) {}
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    template <class T>
+    cudaError_t get(T **p, size_t bytes) {
+        void *q = nullptr;
+        if (n == 8) return cudaErrorMemoryAllocation;
+        const cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, bytes, pool, s) : cudaMallocAsync(&q, bytes, s);
+        if (e != cudaSuccess) return e;
+        ptrs[n++] = q;
+        *p = static_cast<T *>(q);
+        return cudaSuccess;
+    }
+    ~Scratch() {
+        for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], s);
+    }
+};
+
 // Device pointers, asynchronous on s.
 int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, float *dist, cudaStream_t s,
                     unsigned long long *d_stats, const unsigned long long *seed = nullptr,
@@ -497,29 +535,22 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     cudaEvent_t *ev = nullptr;
     if (a->prof_n < a->prof_cap) ev = &a->prof_ev[4 * (a->prof_n++)];
     if (ev) SEG_CUDA(cudaEventRecord(ev[0], s), "seg_classify: profile event");
+    Scratch sc(s, a->pool);
     uint32_t *key = nullptr, *hist = nullptr;
     int32_t *perm = nullptr;
     if (n >= SORT_MIN_N) {
-        SEG_CUDA(cudaMallocAsync((void **)&key, sizeof(uint32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
-        SEG_CUDA(cudaMallocAsync((void **)&perm, sizeof(int32_t) * (size_t)n, s), "seg_classify: cudaMallocAsync");
-        SEG_CUDA(cudaMallocAsync((void **)&hist, sizeof(uint32_t) * morton_scratch_words(), s),
-                 "seg_classify: cudaMallocAsync");
+        SEG_CUDA(sc.get(&key, sizeof(uint32_t) * (size_t)n), "seg_classify: scratch allocation");
+        SEG_CUDA(sc.get(&perm, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
+        SEG_CUDA(sc.get(&hist, sizeof(uint32_t) * morton_scratch_words()), "seg_classify: scratch allocation");
         MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, hist + MORTON_BUCKETS, perm};
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
     uint32_t *tbits = nullptr;
-    SEG_CUDA(cudaMallocAsync((void **)&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T), s),
-             "seg_classify: cudaMallocAsync");
+    SEG_CUDA(sc.get(&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T)), "seg_classify: scratch allocation");
     ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys};
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
-    cudaFreeAsync(tbits, s);
-    if (key) {
-        cudaFreeAsync(key, s);
-        cudaFreeAsync(perm, s);
-        cudaFreeAsync(hist, s);
-    }
     if (e != cudaSuccess) return cuda_fail(e, "seg_classify: kernel launch");
     return SEG_OK;
 }
@@ -571,9 +602,12 @@ int classify_host(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab,
     int rc = SEG_OK;
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < nb && e == cudaSuccess; ++i) {
-        e = cudaMallocAsync((void **)&dfib[i], sizeof(float) * 3 * NPTS * cap, s);
-        if (e == cudaSuccess) e = cudaMallocAsync((void **)&dlab[i], sizeof(int32_t) * cap, s);
-        if (e == cudaSuccess) e = cudaMallocAsync((void **)&ddist[i], sizeof(float) * cap, s);
+        auto get = [&](void **p, size_t bytes) {
+            return a->pool ? cudaMallocFromPoolAsync(p, bytes, a->pool, s) : cudaMallocAsync(p, bytes, s);
+        };
+        e = get((void **)&dfib[i], sizeof(float) * 3 * NPTS * cap);
+        if (e == cudaSuccess) e = get((void **)&dlab[i], sizeof(int32_t) * cap);
+        if (e == cudaSuccess) e = get((void **)&ddist[i], sizeof(float) * cap);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
