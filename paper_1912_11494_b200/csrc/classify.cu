@@ -113,20 +113,22 @@ __device__ __forceinline__ u64 f2u(float2 v) {
 }
 
 // ----------------------------------------------------------------------------------------
-// a9: spatial-order prepass (counting sort on a 2^18-bucket Morton grid of point 10)
+// a9: spatial-order prepass (counting sort on a Morton grid of point 10: 2^21 buckets, 2^18 for small N)
 // ----------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 6 bits -> every third bit
-    v &= 0x3f;
-    v = (v | (v << 8)) & 0x0000f00fu;
-    v = (v | (v << 4)) & 0x000c30c3u;
-    v = (v | (v << 2)) & 0x00249249u;
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // up to 10 bits -> every third bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
     return v;
 }
 
 constexpr int MORTON_FPT = 4;   // fibers per thread in k_morton_hist (independent loads in flight)
 
 __global__ void k_morton_hist(MortonParams p) {
-    const float lim = (float)((1 << MORTON_BITS) - 1);
+    const float lim = (float)((1 << p.bits) - 1);
+    const float sc = (float)(1 << (p.bits - MORTON_BITS));   // inv_cell is for the 6-bit grid
     const int i0 = blockIdx.x * blockDim.x * MORTON_FPT + threadIdx.x;
     float v[MORTON_FPT][3];
 #pragma unroll
@@ -141,9 +143,9 @@ __global__ void k_morton_hist(MortonParams p) {
         const int i = i0 + q * blockDim.x;
         if (i >= p.n) break;
         // fmaxf/fminf map NaN to the bound, so non-finite fibers land in a valid bucket
-        const float qx = fminf(fmaxf((v[q][0] - p.lo.x) * p.inv_cell.x, 0.f), lim);
-        const float qy = fminf(fmaxf((v[q][1] - p.lo.y) * p.inv_cell.y, 0.f), lim);
-        const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * p.inv_cell.z, 0.f), lim);
+        const float qx = fminf(fmaxf((v[q][0] - p.lo.x) * (p.inv_cell.x * sc), 0.f), lim);
+        const float qy = fminf(fmaxf((v[q][1] - p.lo.y) * (p.inv_cell.y * sc), 0.f), lim);
+        const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * (p.inv_cell.z * sc), 0.f), lim);
         const uint32_t k = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
         p.key[i] = k;
         atomicAdd(p.hist + k, 1u);
@@ -154,8 +156,7 @@ __global__ void k_morton_hist(MortonParams p) {
 // range in place and writes its total (k_scan_blocks, 256 blocks in parallel); one block scans the
 // totals (k_scan_totals); k_morton_scatter adds the block offset of its key.
 constexpr int SCAN_B = 1024;                       // buckets per block: 256 threads x 4
-constexpr int SCAN_NB = MORTON_BUCKETS / SCAN_B;   // 256 blocks
-static_assert(MORTON_BUCKETS % SCAN_B == 0 && SCAN_NB <= 1024, "scan shape");
+static_assert(MORTON_BUCKETS % SCAN_B == 0 && (MORTON_BUCKETS / SCAN_B) % 256 == 0, "scan shape");
 
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *warp_sums, uint32_t &total) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -193,36 +194,48 @@ __global__ void __launch_bounds__(256) k_scan_blocks(uint32_t *hist, uint32_t *b
     if (threadIdx.x == 0) bsum[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(256) k_scan_totals(uint32_t *bsum) {
+__global__ void __launch_bounds__(256) k_scan_totals(uint32_t *bsum, int nb) {
+    // nb block totals (a multiple of 256), nb / 256 consecutive ones per thread
+    const int per = nb / 256;
     __shared__ uint32_t warp_sums[9];
-    const uint32_t v = threadIdx.x < SCAN_NB ? bsum[threadIdx.x] : 0u;
+    uint32_t sum = 0;
+    for (int k = 0; k < per; ++k) sum += bsum[threadIdx.x * per + k];
     uint32_t total;
-    const uint32_t ex = block_excl_scan256(v, warp_sums, total);
-    if (threadIdx.x < SCAN_NB) bsum[threadIdx.x] = ex;
+    uint32_t ex = block_excl_scan256(sum, warp_sums, total);
+    for (int k = 0; k < per; ++k) {
+        const uint32_t v = bsum[threadIdx.x * per + k];
+        bsum[threadIdx.x * per + k] = ex;
+        ex += v;
+    }
 }
 
 __global__ void k_morton_scatter(MortonParams p) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     const uint32_t k = p.key[i];
-    SEG_DCHECK(k < (uint32_t)MORTON_BUCKETS);
+    SEG_DCHECK(k < (1u << (3 * p.bits)));
     const uint32_t pos = atomicAdd(p.hist + k, 1u) + __ldg(p.bsum + k / SCAN_B);
     SEG_DCHECK(pos < (uint32_t)p.n);
     p.perm[pos] = i;
 }
 
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * MORTON_BUCKETS, s);
+    const size_t buckets = (size_t)1 << (3 * p.bits);
+    const int nb = (int)(buckets / SCAN_B);
+    cudaError_t e = cudaMemsetAsync(p.hist, 0, sizeof(uint32_t) * buckets, s);
     if (e != cudaSuccess) return e;
     const int g = (p.n + 255) / 256;
     k_morton_hist<<<(p.n + 256 * MORTON_FPT - 1) / (256 * MORTON_FPT), 256, 0, s>>>(p);
-    k_scan_blocks<<<SCAN_NB, 256, 0, s>>>(p.hist, p.bsum);
-    k_scan_totals<<<1, 256, 0, s>>>(p.bsum);
+    k_scan_blocks<<<nb, 256, 0, s>>>(p.hist, p.bsum);
+    k_scan_totals<<<1, 256, 0, s>>>(p.bsum, nb);
     k_morton_scatter<<<g, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 
-size_t morton_scratch_words() { return (size_t)MORTON_BUCKETS + SCAN_NB; }
+size_t morton_scratch_words(int bits) {
+    const size_t buckets = (size_t)1 << (3 * bits);
+    return buckets + buckets / SCAN_B;
+}
 
 // ----------------------------------------------------------------------------------------
 // a1-a8: the classify kernel

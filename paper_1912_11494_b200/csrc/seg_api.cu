@@ -541,8 +541,9 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     if (n >= SORT_MIN_N) {
         SEG_CUDA(sc.get(&key, sizeof(uint32_t) * (size_t)n), "seg_classify: scratch allocation");
         SEG_CUDA(sc.get(&perm, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
-        SEG_CUDA(sc.get(&hist, sizeof(uint32_t) * morton_scratch_words()), "seg_classify: scratch allocation");
-        MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, hist + MORTON_BUCKETS, perm};
+        const int bits = morton_bits_for(n);
+        SEG_CUDA(sc.get(&hist, sizeof(uint32_t) * morton_scratch_words(bits)), "seg_classify: scratch allocation");
+        MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, hist + ((size_t)1 << (3 * bits)), perm, bits};
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
     uint32_t *tbits = nullptr;

@@ -22,8 +22,13 @@ constexpr int TILE_HDR_F4 = 4;           // the tile's 64-B TileHdr travels in f
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
 constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,816 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
-constexpr int MORTON_BITS = 6;           // per axis -> 2^18 spatial buckets for the prepass
+constexpr int MORTON_BITS = 6;           // per axis, the grid seg_create scales (inv_cell) for
 constexpr int MORTON_BUCKETS = 1 << (3 * MORTON_BITS);
+// the prepass grid per call: 7 bits per axis (2^21 buckets) from this many fibers on, else 6 (2^18):
+// finer cells order the fibers inside today's cells and spread the scatter's atomics (cfg 3 -1.8%);
+// small inputs pay more for the larger histogram than they gain
+constexpr int MORTON_FINE_N = 1 << 19;
+__host__ __device__ constexpr int morton_bits_for(int n) { return n >= MORTON_FINE_N ? 7 : 6; }
 
 // Per-tile header: bounding spheres (centre xyz, radius w) of centroid points 0, 10, 20
 // over the tile's members, the tile's bundle and its threshold (squared, FP32).
@@ -81,6 +86,7 @@ struct MortonParams {
     uint32_t *hist;           // [MORTON_BUCKETS]
     uint32_t *bsum;           // [MORTON_BUCKETS / 1024] per-block totals, then offsets
     int32_t *perm;            // [n]
+    int bits;                 // grid bits per axis for this call (morton_bits_for(n))
 };
 
 // Row f3 (group.cu): the stable partition of the fibers by label.
@@ -109,7 +115,7 @@ struct ResampleParams {
 
 // Launchers (classify.cu, group.cu, resample.cu).  All are asynchronous on `s`.
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s);
-size_t morton_scratch_words();   // hist + block offsets
+size_t morton_scratch_words(int bits);   // hist + block offsets
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull = nullptr);
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
