@@ -74,7 +74,7 @@ def test_paper_cfg1_subset_parity():
     check_parity(lab, d, ref, "cfg1[:4000] paper")
 
 
-@pytest.mark.parametrize("cfg,k", [(3, 300), (4, 300)])
+@pytest.mark.parametrize("cfg,k", [(3, 2000), (4, 2000)])
 def test_paper_full_size_sampled(cfg, k):
     """Full-size subject (launched as bench.py launches it), compared on a seeded sample."""
     at = atlas_for_config(cfg)

@@ -79,7 +79,7 @@ def test_cfg1_subset_full_parity():
     check_parity(lab, d, ref, "cfg1[:6000]")
 
 
-@pytest.mark.parametrize("cfg,k", [(1, 1500), (2, 600), (3, 300), (4, 300)])
+@pytest.mark.parametrize("cfg,k", [(1, 5000), (2, 3000), (3, 3000), (4, 3000)])
 def test_full_size_sampled_parity(cfg, k):
     """BASELINE.json configs at full size, launched like bench.py; sampled oracle check."""
     at = atlas_for_config(cfg)
