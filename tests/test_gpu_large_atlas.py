@@ -47,3 +47,33 @@ def test_large_atlas_parity(big):
     # the same answer through the host-buffer pipeline
     hl, hd = A.classify(fib)
     assert np.array_equal(hl, lab.cpu().numpy()) and np.array_equal(hd.view(np.int32), d.cpu().numpy().view(np.int32))
+
+
+def _one_centroid_bundles(nb, seed):
+    """nb bundles of one centroid each (one tile each): centroids drawn from config 3's atlas, jittered."""
+    at = atlas_for_config(3)
+    rng = np.random.default_rng(seed)
+    pick = rng.integers(0, at.M, size=nb)
+    cents = (at.centroids[pick] + rng.normal(0, 1.0, size=(nb, 1, 3))).astype(np.float32)
+    return (np.ascontiguousarray(cents), np.arange(nb, dtype=np.int32),
+            np.ascontiguousarray(rng.uniform(5, 10, nb).astype(np.float32)))
+
+
+def test_max_tiles_atlas_parity_and_limit():
+    """Exactly the build's tile limit (30,000 tiles) works and matches the oracle; one more is refused."""
+    from paper_1912_11494_b200 import Atlas, binding
+    cents, bid, thr = _one_centroid_bundles(30000, 7)
+    A = Atlas(*(torch.from_numpy(x).cuda() for x in (cents, bid, thr)))
+    assert A.info["n_tiles"] == 30000
+    full = fibers_for_config(3, 0, 100000)
+    fib = np.ascontiguousarray(full[sample_indices(len(full), 5000, seed=45)])
+    lab, d = A.classify(torch.from_numpy(fib).cuda())
+    torch.cuda.synchronize()
+    ref = oracle.classify(fib[:500], cents, bid, thr)
+    info = check_parity(lab.cpu().numpy()[:500], d.cpu().numpy()[:500], ref, "30000-tile atlas")
+    assert info["labelled"] > 50
+    A.close()
+    c2, b2, t2 = _one_centroid_bundles(30001, 8)
+    with pytest.raises(binding.SegError) as ei:
+        Atlas(*(torch.from_numpy(x).cuda() for x in (c2, b2, t2)))
+    assert ei.value.code == binding.SEG_EINVAL and "30001 tiles" in str(ei.value)
