@@ -353,16 +353,22 @@ __device__ __forceinline__ float tn_f32(float ls, float lc) {
     return __fsub_rn(__fmul_rn(q, q), 1.f);
 }
 
-// a2: exact tile lower bound: for every centroid c of the tile,
-// d_ME >= |f10 - c10| >= |f10 - C10| - R10 and d_ME >= min over orientations of the end-point
-// maximum, each term bounded the same way.  Skip iff the bound exceeds s = sqrt(tau) + CULL_EPS.
+// a2: exact tile lower bound
+// squared distance from point (x, y, z) to the box [lo, hi] (0 inside), FP32
+__device__ __forceinline__ float box_d2(float x, float y, float z, const float4 &lo, const float4 &hi) {
+    const float dx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.f);
+    const float dy = fmaxf(fmaxf(lo.y - y, y - hi.y), 0.f);
+    const float dz = fmaxf(fmaxf(lo.z - z, z - hi.z), 0.f);
+    return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+// a2 with boxes: for every centroid c of the tile, |f_p - c_p| >= dist(f_p, box_p) (c_p lies in box_p);
+// the same orientation logic as the spheres.  Skip iff the bound exceeds s = sqrt(tau) + CULL_EPS.
 __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez, const float4 &F10,
                                               const TileHdr &h, float s) {
-    const float r0 = h.s0.w + s, r10 = h.s10.w + s, r20 = h.s20.w + s;
-    const float a0 = r0 * r0, a10 = r10 * r10, a20 = r20 * r20;
-    const bool p10 = d2(F10.x, F10.y, F10.z, h.s10) <= a10;
-    const bool pdir = d2(E.x, E.z, Ez.x, h.s0) <= a0 && d2(E.y, E.w, Ez.y, h.s20) <= a20;
-    const bool pinv = d2(E.x, E.z, Ez.x, h.s20) <= a20 && d2(E.y, E.w, Ez.y, h.s0) <= a0;
+    const float s2 = s * s;
+    const bool p10 = box_d2(F10.x, F10.y, F10.z, h.lo10, h.hi10) <= s2;
+    const bool pdir = box_d2(E.x, E.z, Ez.x, h.lo0, h.hi0) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo20, h.hi20) <= s2;
+    const bool pinv = box_d2(E.x, E.z, Ez.x, h.lo20, h.hi20) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo0, h.hi0) <= s2;
     return p10 && (pdir || pinv);
 }
 

@@ -393,13 +393,33 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
         }
         const float *s = &P.spheres[(size_t)t * 12];
         const int b = P.tile_bundle[t];
-        th[t].s0 = make_float4(s[0], s[1], s[2], s[3]);
-        th[t].s10 = make_float4(s[4], s[5], s[6], s[7]);
-        th[t].s20 = make_float4(s[8], s[9], s[10], s[11]);
         th[t].bundle = b;
         th[t].thr = thr[b];
         th[t].thr2 = thr[b] * thr[b];
         th[t].pad = 0;
+        {   // the boxes of points 0, 10, 20 over the tile's members (padding slots repeat a member)
+            float blo[3][3], bhi[3][3];
+            for (int q = 0; q < 3; ++q)
+                for (int d = 0; d < 3; ++d) { blo[q][d] = INFINITY; bhi[q][d] = -INFINITY; }
+            for (int k = 0; k < TILE; ++k) {
+                const int m = P.members[(size_t)t * TILE + k];
+                const int pts[3] = {0, 10, 20};
+                for (int q = 0; q < 3; ++q) {
+                    const int src = P.flipped[m] ? (NPTS - 1 - pts[q]) : pts[q];
+                    const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
+                    for (int d = 0; d < 3; ++d) {
+                        blo[q][d] = std::min(blo[q][d], c[d]);
+                        bhi[q][d] = std::max(bhi[q][d], c[d]);
+                    }
+                }
+            }
+            th[t].lo0 = make_float4(blo[0][0], blo[0][1], blo[0][2], 0.f);
+            th[t].hi0 = make_float4(bhi[0][0], bhi[0][1], bhi[0][2], 0.f);
+            th[t].lo10 = make_float4(blo[1][0], blo[1][1], blo[1][2], 0.f);
+            th[t].hi10 = make_float4(bhi[1][0], bhi[1][1], bhi[1][2], 0.f);
+            th[t].lo20 = make_float4(blo[2][0], blo[2][1], blo[2][2], 0.f);
+            th[t].hi20 = make_float4(bhi[2][0], bhi[2][1], bhi[2][2], 0.f);
+        }
         {
             const double sv = (double)thr[b] + (double)CULL_EPS;
             ct[t].c0 = make_float4(s[0], s[1], s[2], sq_up((double)s[3] + sv));

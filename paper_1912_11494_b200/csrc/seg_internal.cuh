@@ -18,7 +18,7 @@ namespace seg {
 constexpr int NPTS = 21;                 // points per fiber / centroid
 constexpr int TILE = 32;                 // centroids per tile (one bit per centroid in a u32 mask)
 constexpr int TILE_F4 = NPTS * TILE;     // float4 of tile point data: [21 points][32 centroids]
-constexpr int TILE_HDR_F4 = 4;           // the tile's 64-B TileHdr travels in front of its data
+constexpr int TILE_HDR_F4 = 7;           // the tile's 112-B TileHdr travels in front of its data
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
 constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,816 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
@@ -30,16 +30,18 @@ constexpr int MORTON_BUCKETS = 1 << (3 * MORTON_BITS);
 constexpr int MORTON_FINE_N = 1 << 19;
 __host__ __device__ constexpr int morton_bits_for(int n) { return n >= MORTON_FINE_N ? 7 : 6; }
 
-// Per-tile header: bounding spheres (centre xyz, radius w) of centroid points 0, 10, 20
-// over the tile's members, the tile's bundle and its threshold (squared, FP32).
+// Per-tile header: the tile's bundle and threshold (FP32, squared too), and the axis-aligned boxes of
+// centroid points 0, 10, 20 over the tile's members (exact FP32 min / max, canonical orientation): the
+// live tile bound of k_classify.  Boxes leave 0.59-0.81 of the spheres' (fiber, tile) passes at the live
+// cutoff; k_cull keeps spheres (CullTile) for its threshold-only list.
 struct __align__(16) TileHdr {
-    float4 s0, s10, s20;
     int bundle;
     float thr2;
     float thr;
     int pad;
+    float4 lo0, hi0, lo10, hi10, lo20, hi20;
 };
-static_assert(sizeof(TileHdr) == 64, "TileHdr is 64 B");
+static_assert(sizeof(TileHdr) == 16 * TILE_HDR_F4, "TileHdr fills TILE_HDR_F4 float4");
 
 // k_cull's copy of a tile's bounds, squared and grown once at seg_create: c0 / c10 / c20 = sphere centre
 // of points 0 / 10 / 20 with w = (radius + thr + CULL_EPS)^2 (the threshold-only bound, rounded up in
