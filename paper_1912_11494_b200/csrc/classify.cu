@@ -271,9 +271,11 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
 #ifndef SEG_FB
-#define SEG_FB 4
+#define SEG_FB 3
 #endif
-constexpr int FB = SEG_FB;             // fibers per step of the dense test1+test2 loop (cfg 3: 3 -> +1%, 5 -> +3%, 8 -> +16%)
+// fibers per step of the dense test1+test2 loop: with the box bound a warp-tile holds ~11 passing fibers,
+// and 3 wastes fewer slots in the last step than 4 (cfg 3: 4 -> +0.8%, 2 -> +1.2%, 5 -> +4.6%)
+constexpr int FB = SEG_FB;
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
