@@ -79,9 +79,8 @@ def simulate(ctas):
                     if d2<=tau: best=np.sqrt(d2)
             nf+=1
     return hits/nf, full/nf, npass/nf, nlist/len(ctas)
-ctasM=[np.arange(k*256,(k+1)*256) for k in range(32)]
-o2=np.lexsort((mkey[win], near))
-ctasN=[o2[k*256:(k+1)*256] for k in range(32)]
+near10=np.argmin(bd(f10,1),1)
+o5=np.lexsort((mkey[win], near10))
+ctasP=[o5[k*256:(k+1)*256] for k in range(32)]
 print("same 8192 fibers, all 32 CTAs of the window")
-print("Morton CTAs:       hits/fiber %.3f  full evals/fiber %.3f  box passes/fiber %.2f  listed tiles/CTA %.1f" % simulate(ctasM))
-print("nearest-tile CTAs: hits/fiber %.3f  full evals/fiber %.3f  box passes/fiber %.2f  listed tiles/CTA %.1f" % simulate(ctasN))
+print("point-10-nearest-tile CTAs: hits/fiber %.3f  full evals/fiber %.3f  box passes/fiber %.2f  listed tiles/CTA %.1f" % simulate(ctasP))
