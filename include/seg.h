@@ -58,8 +58,9 @@ typedef struct seg_atlas seg_atlas;
  * seg_create -- build an atlas context on `device` (-1 = the calling thread's current
  * device).  Groups centroids by bundle (the paper's atlasData[j]),
  * orders each bundle spatially, cuts it into tiles of 32 centroids that never cross a
- * bundle, and uploads the tiles plus per-tile / per-bundle bounding spheres of
- * points 0, 10 and 20 (the exact lower bounds of the cull).
+ * bundle, and uploads the tiles plus per-tile / per-bundle bounding spheres and per-tile
+ * axis-aligned boxes of points 0, 10 and 20 (the exact lower bounds of the cull: spheres for
+ * the per-CTA tile lists, boxes for the live per-fiber test).
  *   centroids  float32 [M][21][3], host or device memory (detected)
  *   bundle_id  int32 [M] in [0, B), host or device memory
  *   M >= 1, B >= 1; thresh float32 [B], finite and > 0 (host or device memory)
@@ -129,8 +130,8 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
  *   [3] (lane, tile) pairs passing the tile bound    [4] lane midpoint tests (test1)
  *   [5] lane endpoint tests (test2)                  [6] lane orientation passes into test3/4
  *   [7] lane full 21-point completions               [8] best-distance updates (Alg. 1 l.15-16)
- *   [9] lane point-distance evaluations (Eq. 1, all stages and the sphere bounds)
- *   [10] lane sphere-bound tests (bundle + tile)     [11] CTAs
+ *   [9] lane point-distance evaluations (Eq. 1, all stages and the bounds)
+ *   [10] lane tile-bound tests (live, boxes)         [11] CTAs
  *   clock64 cycles summed over consumer warps: [12] tile loop, [13] waiting for a tile,
  *   [14] best-first candidate selection (incl. the candidate rounds it triggers),
  *   [15] candidate rounds, [16] live tile-bound test, [17] fiber ingest (start -> first barrier)
