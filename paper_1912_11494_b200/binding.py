@@ -18,7 +18,7 @@ SEG_KEY_NONE, SEG_KEY_NONFINITE = 0x7FFFFFFFFFFFFFFF, 0x7FFFFFFFFFFFFFFE
 SEG_NSTATS = 22
 STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_pass", "lane_test1",
               "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
-              "lane_sphere_tests", "ctas",
+              "lane_bound_tests", "ctas",
               "cyc_consumer", "cyc_full_wait", "cyc_hit_select", "cyc_cand_rounds", "cyc_tile_test", "cyc_ingest",
               "rounds", "round_lanes", "hit_fibers", "winner_rounds")
 
