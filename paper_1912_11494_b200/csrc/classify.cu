@@ -491,6 +491,33 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
     __syncthreads();
+    // the seed (exact mode): k_cull named for each fiber the best-first winner of its nearest tile; the lane
+    // evaluates that one candidate in full -- its fiber from shared memory, the centroid's 21 points from
+    // the centroid-major copy -- with k_classify's arithmetic, and starts from its key.  It is one of the
+    // candidates the tile stream would evaluate, so the result cannot change; a good start prunes the rest.
+    if (!PAPER && consumer && p.seed_code && inrange && fm[lane].w != 0.f) {
+        const int code = __ldg(p.seed_code + fidx);
+        if (code >= 0) {
+            const int tn = code >> 6, c = (code >> 1) & 31, o = code & 1;
+            const float4 *cc = p.tiles_cm + ((size_t)tn * TILE + c) * NPTS;
+            const TileHdr *h = reinterpret_cast<const TileHdr *>(p.tiles + (size_t)tn * TILE_STRIDE_F4);
+            const float4 E = fe[lane], F10 = fm[lane];
+            const float2 Ez = fez[lane];
+            float r = d2(F10.x, F10.y, F10.z, __ldg(cc + 10));
+            r = fmaxf(r, d2(E.x, E.z, Ez.x, __ldg(cc + (o ? NPTS - 1 : 0))));
+            r = fmaxf(r, d2(E.y, E.w, Ez.y, __ldg(cc + (o ? 0 : NPTS - 1))));
+#pragma unroll
+            for (int i = 1; i < NPTS - 1; ++i) {
+                if (i == 10) continue;
+                const float2 a = fxy[mid_slot(i) * 32 + lane];
+                r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + lane], __ldg(cc + (o ? NPTS - 1 - i : i))));
+            }
+            if (r <= __ldg(&h->thr2)) {
+                const unsigned long long kk = ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)__ldg(&h->bundle);
+                if (kk < best[lane]) best[lane] = kk;
+            }
+        }
+    }
     if (STATS && consumer && lane == 0) cnt[ST_CYC_INGEST] += clock64() - ti0;
 
     if (!consumer) {
@@ -815,6 +842,8 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
              isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
     }
     if (!ok) F10 = make_float4(__int_as_float(0x7fffffff), 0.f, 0.f, 0.f);   // NaN: every bound test fails
+    float nd2 = INFINITY;   // each fiber's nearest tile by its sphere centres: the seed's tile
+    int ntile = -1;
     __syncthreads();
     // bundles some fiber of the CTA may need (point-10 sphere + threshold, exact)
     for (int b0 = 0; b0 < p.B; b0 += 32) {
@@ -856,6 +885,8 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
                                            ((d00 <= ct.q.x && d2020 <= ct.q.z) || (d020 <= ct.q.z && d200 <= ct.q.x));
                         pm |= (pass ? 1u : 0u) << j;
                         cm |= (close ? 1u : 0u) << j;
+                        const float dc = fmaxf(d10, fminf(fmaxf(d00, d2020), fmaxf(d020, d200)));
+                        if (pass && dc < nd2) { nd2 = dc; ntile = t0 + j; }
                     }
                 }
                 // transpose: lane j gets the pass / inside counts of tile t0 + j over the warp,
@@ -875,6 +906,50 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
                     atomicAdd(prio + t, (uint32_t)nclose * 256u + (uint32_t)npass);
                 }
             }
+        }
+    }
+    // the seed candidate (exact mode): per fiber, the best-first winner of its nearest tile (smallest 3-point
+    // score), named as (tile, centroid, orientation) for k_classify, which evaluates it in full and starts
+    // from it.  Warp-cooperative: lane = centroid for the 3-point scores (the tile's rows stay in registers
+    // while consecutive fibers share the tile); only points 0 / 10 / 20, already in registers, are needed.
+    if (p.seed_code) {
+        const int myfidx = gi < p.n ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
+        const bool want = myfidx >= 0 && ntile >= 0;
+        if (myfidx >= 0 && !want) p.seed_code[myfidx] = -1;
+        int ct = -1;
+        float thr2 = 0.f;
+        float4 c10 = make_float4(0.f, 0.f, 0.f, 0.f), c0 = c10, c20 = c10;
+        for (uint32_t rem = __ballot_sync(0xffffffffu, want); rem; rem &= rem - 1) {
+            const int j = __ffs(rem) - 1;
+            const int fj = __shfl_sync(0xffffffffu, myfidx, j);
+            const int tj = __shfl_sync(0xffffffffu, ntile, j);
+            if (tj != ct) {
+                ct = tj;
+                const float4 *tile = p.tiles + (size_t)tj * TILE_STRIDE_F4;
+                const TileHdr *h = reinterpret_cast<const TileHdr *>(tile);
+                const float4 *T = tile + TILE_HDR_F4;
+                thr2 = __ldg(&h->thr2);
+                c10 = __ldg(T + 10 * TILE + lane);
+                c0 = __ldg(T + lane);
+                c20 = __ldg(T + 20 * TILE + lane);
+            }
+            const float4 Ej = make_float4(__shfl_sync(0xffffffffu, E.x, j), __shfl_sync(0xffffffffu, E.y, j),
+                                          __shfl_sync(0xffffffffu, E.z, j), __shfl_sync(0xffffffffu, E.w, j));
+            const float2 Ezj = make_float2(__shfl_sync(0xffffffffu, Ez.x, j), __shfl_sync(0xffffffffu, Ez.y, j));
+            const float3 Fj = make_float3(__shfl_sync(0xffffffffu, F10.x, j), __shfl_sync(0xffffffffu, F10.y, j),
+                                          __shfl_sync(0xffffffffu, F10.z, j));
+            const float m10 = d2(Fj.x, Fj.y, Fj.z, c10);
+            const float rd = fmaxf(fmaxf(m10, d2(Ej.x, Ej.z, Ezj.x, c0)), d2(Ej.y, Ej.w, Ezj.y, c20));
+            const float ri = fmaxf(fmaxf(m10, d2(Ej.x, Ej.z, Ezj.x, c20)), d2(Ej.y, Ej.w, Ezj.y, c0));
+            const float sc = fminf(rd <= thr2 ? rd : INFINITY, ri <= thr2 ? ri : INFINITY);
+            const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
+            int32_t code = -1;   // (tile << 6) | (centroid << 1) | orientation of the winner, -1 = none
+            if ((smin & ~31u) < 0x7f800000u) {
+                const int wl = (int)(smin & 31u);
+                const int wo = __shfl_sync(0xffffffffu, (rd <= thr2 && rd == sc) ? 0 : 1, wl);
+                code = (ct << 6) | (wl << 1) | wo;
+            }
+            if (lane == 0) p.seed_code[fj] = code;
         }
     }
     __syncthreads();
@@ -961,7 +1036,8 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
     const size_t cull_smem = sizeof(uint32_t) * (size_t)(((p.T + 31) >> 5) + ((p.B + 31) >> 5) + p.T) +
-                             sizeof(uint16_t) * (size_t)p.T;
+                             sizeof(uint16_t) * (size_t)p.T
+;
     cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
     if (e != cudaSuccess) return e;
     k_cull<<<grid, FPC, cull_smem, s>>>(p);

@@ -48,6 +48,7 @@ struct seg_atlas {
     int B = 0, T = 0;
     int paper = 0;                // SEG_MODE_PAPER: score = d_ME (inferred orientation) + TN
     float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points (point 0's w = chord length)
+    float4 *tiles_cm = nullptr;   // [T][32][21] the same points centroid-major (the seed evaluation's loads)
     TileHdr *th = nullptr;        // [T]
     CullTile *ct = nullptr;       // [T] squared bounds for k_cull
     BundleHdr *bh = nullptr;      // [B]
@@ -308,6 +309,7 @@ static void free_atlas(seg_atlas *a) {
     DeviceGuard g(a->device);
     free_prof(a);
     cudaFree(a->tiles);
+    cudaFree(a->tiles_cm);
     cudaFree(a->th);
     cudaFree(a->ct);
     cudaFree(a->bh);
@@ -353,6 +355,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
 
     // device images
     std::vector<float4> tiles((size_t)P.T * TILE_STRIDE_F4);
+    std::vector<float4> tiles_cm((size_t)P.T * TILE * NPTS);
     // chord length of every centroid's 21-point polyline (Eq. 3's l_C, reading R16), in double
     std::vector<float> clen((size_t)M);
     for (int64_t m = 0; m < M; ++m) {
@@ -385,6 +388,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
                 tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] =
                     make_float4(c[0], c[1], c[2], i == 0 ? clen[(size_t)m] : 0.f);
+                tiles_cm[((size_t)t * TILE + k) * NPTS + i] = make_float4(c[0], c[1], c[2], 0.f);
                 for (int d = 0; d < 3; ++d) {
                     lo[d] = std::min(lo[d], c[d]);
                     hi[d] = std::max(hi[d], c[d]);
@@ -460,6 +464,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
     const size_t bt = tiles.size() * sizeof(float4), bth = th.size() * sizeof(TileHdr),
                  bbh = bh.size() * sizeof(BundleHdr);
     cudaError_t e = cudaMalloc(&a->tiles, bt);
+    if (e == cudaSuccess) e = cudaMalloc(&a->tiles_cm, tiles_cm.size() * sizeof(float4));
     if (e == cudaSuccess) e = cudaMalloc(&a->th, bth);
     if (e == cudaSuccess) e = cudaMalloc(&a->ct, sizeof(CullTile) * ct.size());
     if (e == cudaSuccess) e = cudaMalloc(&a->bh, bbh);
@@ -470,6 +475,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
                     std::string("seg_create: cudaMalloc: ") + cudaGetErrorString(e));
     }
     e = cudaMemcpy(a->tiles, tiles.data(), bt, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(a->tiles_cm, tiles_cm.data(), tiles_cm.size() * sizeof(float4), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(a->th, th.data(), bth, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(a->ct, ct.data(), sizeof(CullTile) * ct.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(a->bh, bh.data(), bbh, cudaMemcpyHostToDevice);
@@ -477,7 +483,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
         free_atlas(a);
         return cuda_fail(e, "seg_create: cudaMemcpy H2D");
     }
-    a->bytes = (int64_t)(bt + bth + bbh + sizeof(CullTile) * ct.size());
+    a->bytes = (int64_t)(bt + bth + bbh + sizeof(CullTile) * ct.size() + tiles_cm.size() * sizeof(float4));
     // a private pool keeps the per-call scratch cached between seg_classify calls without changing the
     // device's default pool; if one cannot be created the default pool is used as it is
     {
@@ -568,7 +574,11 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     }
     uint32_t *tbits = nullptr;
     SEG_CUDA(sc.get(&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T)), "seg_classify: scratch allocation");
-    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys};
+    ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys,
+                      nullptr, a->tiles_cm};
+    if (!a->paper) {   // k_cull names each fiber's seed candidate, k_classify evaluates it (exact mode)
+        SEG_CUDA(sc.get(&cp.seed_code, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
+    }
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);

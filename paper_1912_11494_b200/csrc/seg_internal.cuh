@@ -77,6 +77,8 @@ struct ClassifyParams {
     uint32_t *tile_bits;       // scratch: per CTA of FPC fibers, [count, tiles...] as u16 (cull_stride(T)): k_cull -> k_classify
     int paper;                 // 0 = exact Eq. 2 (north_star), 1 = paper semantics (Eq. 3 TN, inferred orientation)
     unsigned long long *keys;  // nullable [n]: write the best keys (row f4) instead of label / dist
+    int32_t *seed_code;            // nullable [n] by fiber: k_cull's seed candidate, (tile << 6) | (centroid << 1) | o, -1 = none
+    const float4 *tiles_cm;        // [T][32][21] centroid-major copy of the tile points (the seed evaluation)
 };
 
 struct MortonParams {
