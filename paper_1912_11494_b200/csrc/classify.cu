@@ -495,14 +495,22 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     // evaluates that one candidate in full -- its fiber from shared memory, the centroid's 21 points from
     // the centroid-major copy -- with k_classify's arithmetic, and starts from its key.  It is one of the
     // candidates the tile stream would evaluate, so the result cannot change; a good start prunes the rest.
-    if (!PAPER && consumer && p.seed_code && inrange && fm[lane].w != 0.f) {
+    if (consumer && p.seed_code && inrange && fm[lane].w != 0.f) {
         const int code = __ldg(p.seed_code + fidx);
         if (code >= 0) {
-            const int tn = code >> 6, c = (code >> 1) & 31, o = code & 1;
+            const int tn = code >> 6, c = (code >> 1) & 31;
+            int o = code & 1;
             const float4 *cc = p.tiles_cm + ((size_t)tn * TILE + c) * NPTS;
             const TileHdr *h = reinterpret_cast<const TileHdr *>(p.tiles + (size_t)tn * TILE_STRIDE_F4);
             const float4 E = fe[lane], F10 = fm[lane];
             const float2 Ez = fez[lane];
+            if (PAPER) {
+                // paper mode: the orientation the end points infer, decided as in the dense loop (R17)
+                const float4 c0p = __ldg(cc), c20p = __ldg(cc + NPTS - 1);
+                const float e00 = d2(E.x, E.z, Ez.x, c0p), e2020 = d2(E.y, E.w, Ez.y, c20p);
+                const float e020 = d2(E.x, E.z, Ez.x, c20p), e200 = d2(E.y, E.w, Ez.y, c0p);
+                o = fmaxf(e020, e200) < fmaxf(e00, e2020) ? 1 : 0;
+            }
             float r = d2(F10.x, F10.y, F10.z, __ldg(cc + 10));
             r = fmaxf(r, d2(E.x, E.z, Ez.x, __ldg(cc + (o ? NPTS - 1 : 0))));
             r = fmaxf(r, d2(E.y, E.w, Ez.y, __ldg(cc + (o ? 0 : NPTS - 1))));
@@ -512,7 +520,15 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float2 a = fxy[mid_slot(i) * 32 + lane];
                 r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + lane], __ldg(cc + (o ? NPTS - 1 - i : i))));
             }
-            if (r <= __ldg(&h->thr2)) {
+            if (PAPER) {
+                // score = d_ME + TN (Eq. 3), the lengths as the candidate rounds take them
+                const float clen = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + c).w;
+                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[lane], clen));
+                if (sc <= __ldg(&h->thr)) {
+                    const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)__ldg(&h->bundle);
+                    if (kk < best[lane]) best[lane] = kk;
+                }
+            } else if (r <= __ldg(&h->thr2)) {
                 const unsigned long long kk = ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)__ldg(&h->bundle);
                 if (kk < best[lane]) best[lane] = kk;
             }

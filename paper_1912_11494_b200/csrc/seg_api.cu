@@ -576,7 +576,11 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     SEG_CUDA(sc.get(&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T)), "seg_classify: scratch allocation");
     ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys,
                       nullptr, a->tiles_cm};
-    if (!a->paper) {   // k_cull names each fiber's seed candidate, k_classify evaluates it (exact mode)
+#ifndef SEG_NOPAPERSEED
+    {   // k_cull names each fiber's seed candidate, k_classify evaluates it
+#else
+    if (!a->paper) {
+#endif
         SEG_CUDA(sc.get(&cp.seed_code, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
     }
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
