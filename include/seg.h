@@ -157,6 +157,8 @@ int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,
  *                       dsum is accumulated with floating-point atomics: its last bits may vary
  *                       between runs; order, offsets, dmin and dmax are bitwise deterministic.
  * All arrays are device memory on one device; ASYNCHRONOUS on `stream`; 1 <= B <= 4095.
+ * Scratch comes from a stream-ordered pool the library keeps per device (cached between calls; the
+ * device's default pool is not touched).
  * Errors: SEG_EINVAL (N < 0 or > 2^31-1, B out of range, null pointer, host memory, mixed devices),
  * SEG_ECUDA.
  */

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -76,6 +77,33 @@ struct DeviceGuard {  // restores the caller's current device
         if (prev >= 0) cudaSetDevice(prev);
     }
 };
+
+// The library's own stream-ordered pool per device, for the entry points without an atlas
+// (seg_group_by_bundle): created once, kept cached (release threshold: never), so repeated calls do
+// not map fresh memory; the device's default pool is left as the caller configured it.  nullptr if a
+// pool cannot be created (the default pool is used then).
+cudaMemPool_t lib_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    static bool tried[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!tried[dev]) {
+        tried[dev] = true;
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) == cudaSuccess) {
+            uint64_t thr_bytes = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr_bytes);
+        } else {
+            pools[dev] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    return pools[dev];
+}
 
 // 1 = device (or managed) memory, 0 = host memory, -1 = CUDA unavailable
 int pointer_kind(const void *p, int *dev) {
@@ -730,8 +758,9 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
     }
     unsigned long long *d_stats = nullptr;
     if (stats) {
-        SEG_CUDA(cudaMallocAsync((void **)&d_stats, sizeof(unsigned long long) * SEG_NSTATS, s),
-                 "seg_classify_stats: cudaMallocAsync");
+        const size_t bytes = sizeof(unsigned long long) * SEG_NSTATS;
+        SEG_CUDA(a->pool ? cudaMallocFromPoolAsync((void **)&d_stats, bytes, a->pool, s) : cudaMallocAsync((void **)&d_stats, bytes, s),
+                 "seg_classify_stats: scratch allocation");
         SEG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * SEG_NSTATS, s),
                  "seg_classify_stats: memset");
     }
@@ -792,7 +821,12 @@ extern "C" int seg_group_by_bundle(const int32_t *label, const float *dist, int6
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *scratch = nullptr;
     const size_t words = group_scratch_words(N, B);
-    SEG_CUDA(cudaMallocAsync((void **)&scratch, sizeof(uint32_t) * words, s), "seg_group_by_bundle: cudaMallocAsync");
+    {
+        cudaMemPool_t pool = lib_pool(dev);
+        const size_t bytes = sizeof(uint32_t) * words;
+        SEG_CUDA(pool ? cudaMallocFromPoolAsync((void **)&scratch, bytes, pool, s) : cudaMallocAsync((void **)&scratch, bytes, s),
+                 "seg_group_by_bundle: scratch allocation");
+    }
     GroupParams gp{};
     gp.label = label;
     gp.dist = summ ? dist : nullptr;
