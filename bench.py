@@ -32,7 +32,11 @@ sys.path.insert(0, ROOT)
 METRIC = "fiber–centroid comparisons/sec"
 UNIT = "comparisons/s"
 FP32_LANES_PER_SM = 128          # B200 SM: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / guide)
-FP32_INSTR_PER_PDIST = 6         # Eq. 1 squared: 3 FADD + 1 FMUL + 2 FFMA
+FP32_INSTR_PER_PDIST = 6
+# per-fiber algorithmic FP32 work under the tightest exact pruning the survey assumed
+# (≈ 2.5 k / 14.8 k / 18.4 k lane-instructions per fiber, configs 1/3/4).  Fixed per config, so unlike the
+# measured-W fraction it does not fall when a better bound prunes more work.
+SURVEY_INSTR_PER_FIBER = {1: 2.5e3, 3: 14.8e3, 4: 18.4e3}         # Eq. 1 squared: 3 FADD + 1 FMUL + 2 FFMA
 
 
 def parse():
@@ -270,6 +274,11 @@ def main():
                                f"(median SM clock during the timed region)",
                     work_basis=f"{FP32_INSTR_PER_PDIST} FP32 instr x {st['lane_point_dists']:,} lane point-distance "
                                f"evaluations the kernel's rules needed (stats kernel, rank 0 subject)")
+    if cfg in SURVEY_INSTR_PER_FIBER:
+        w_fix = SURVEY_INSTR_PER_FIBER[cfg] * N
+        roofline["frac_survey_work"] = w_fix / (cls_ms * 1e-3) / 1e12 / peak
+        roofline["survey_work_basis"] = (f"SURVEY.md §8(d) fixed {SURVEY_INSTR_PER_FIBER[cfg]:,.0f} FP32 lane-instr "
+                                         f"per fiber x {N:,} fibers (secondary; frac above is primary)")
 
     # ---------------- end to end: host buffers through the public API ----------------
     e2e = None
