@@ -692,12 +692,20 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                     uint32_t hit = 0;
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
-                        jj[q] = pm ? __ffs(pm) - 1 : -1;
-                        pm &= pm - 1;
+                        // highest set bit first: FLO gives the index directly, and -1 once pm is empty
+                        // (the order of a tile's fibers never changes a result: the best is a
+                        // lexicographic minimum)
+                        uint32_t bit;
+                        asm("bfind.u32 %0, %1;" : "=r"(jj[q]) : "r"(pm));       // FLO: -1 if pm == 0
+                        asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(jj[q]));     // PTX clamps: 0 for -1
+                        pm &= ~bit;
                     }
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
-                        const int j = jj[q] < 0 ? 0 : jj[q];
+                        // an empty slot (-1) reads the word just before fe / fm / fez (in the same
+                        // shared-memory block: fz, fe, fm come first) and lane 31's cutoff; its
+                        // result is discarded by the jj >= 0 test below
+                        const int j = jj[q];
                         // fiber j's end points arrive packed: (x0, x20), (y0, y20), (z0, z20)
                         const float4 E = fe[j];
                         const float2 Ez = fez[j];
