@@ -112,6 +112,34 @@ __device__ __forceinline__ u64 f2u(float2 v) {
     return r;
 }
 
+// -DSEG_NOSCREEN: exact mode's dense loop in the d2 form (tests/test_gpu_screen.py requires the same bits)
+#ifdef SEG_NOSCREEN
+constexpr bool SCREEN_OFF = true;
+#else
+constexpr bool SCREEN_OFF = false;
+#endif
+// Exact mode's dot-product screen (seg_internal.cuh): h = (s + ...) - a.c for the two fiber points packed
+// in (px, py, pz) against the scalar centroid point q, s = the packed sums of the lowered half norms.
+// Never above d2 / 2 (see there).
+__device__ __forceinline__ float2 screen_pair_b(u64 px, u64 py, u64 pz, float qx, float qy, float qz, u64 s) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pz), "l"(pk2(-qz, -qz)), "l"(s));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(py), "l"(pk2(-qy, -qy)), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(px), "l"(pk2(-qx, -qx)), "l"(r));
+    return upk2(r);
+}
+__device__ __forceinline__ u64 add_pair_b(u64 a, float b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(pk2(b, b)));
+    return r;
+}
+// the fiber side's lowered half squared norm, FP32 (at most 5u of its own error; seg_internal.cuh)
+__device__ __forceinline__ float screen_half_norm(float x, float y, float z) {
+    if (!(fabsf(x) <= SCREEN_SAFE && fabsf(y) <= SCREEN_SAFE && fabsf(z) <= SCREEN_SAFE)) return -INFINITY;
+    const float h = __fmul_rn(__fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x))), 0.5f);
+    return __fsub_rn(__fmaf_rn(h, -0x1p-18f, h), 0x1p-62f);
+}
+
 // ----------------------------------------------------------------------------------------
 // a9: spatial-order prepass (counting sort on a Morton grid of point 10: 2^21 buckets, 2^18 for small N)
 // ----------------------------------------------------------------------------------------
@@ -270,12 +298,15 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 #define SEG_STAGES 3
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
+// fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
+// the dot-product screen: 2 (cfg 3: 3 -> +1.3%, 4 -> +1.1%, 1 -> +5.4%; the screen's shorter chains
+// make the smaller step pay).  Paper mode, d2 form: 3 (the d2 form at 2: +0.4%, at 4: +0.8%).
 #ifndef SEG_FB
-#define SEG_FB 3
+#define SEG_FB 2
 #endif
-// fibers per step of the dense test1+test2 loop: with the box bound a warp-tile holds ~11 passing fibers,
-// and 3 wastes fewer slots in the last step than 4 (cfg 3: 4 -> +0.8%, 2 -> +1.2%, 5 -> +4.6%)
-constexpr int FB = SEG_FB;
+#ifndef SEG_FB_PAPER
+#define SEG_FB_PAPER 3
+#endif
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
 constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
@@ -307,8 +338,8 @@ struct SmemLayout {
         fxy = o;  o += (size_t)NCW * NMID * 32 * sizeof(float2);
         fz = o;   o += (size_t)NCW * NMID * 32 * sizeof(float);
         fe = o;   o += (size_t)FPC * sizeof(float4);   // (x0, x20, y0, y20)
-        fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = 1 if the fiber is finite
-        fez = o;  o += (size_t)FPC * sizeof(float2);   // (z0, z20)
+        fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = h10 (NaN: a non-finite fiber)
+        fez = o;  o += (size_t)FPC * sizeof(float4);   // (z0, z20, h0, h20): h = lowered half norms
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
         flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
@@ -384,7 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     StageMeta *meta = reinterpret_cast<StageMeta *>(smem + L.meta);
     float4 *fe_all = reinterpret_cast<float4 *>(smem + L.fe);
     float4 *fm_all = reinterpret_cast<float4 *>(smem + L.fm);
-    float2 *fez_all = reinterpret_cast<float2 *>(smem + L.fez);
+    float4 *fez_all = reinterpret_cast<float4 *>(smem + L.fez);
     unsigned long long *best_all = reinterpret_cast<unsigned long long *>(smem + L.best);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -394,7 +425,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NMID * 32);       // [18][32]
     float4 *fe = fe_all + cw * 32;
     float4 *fm = fm_all + cw * 32;
-    float2 *fez = fez_all + cw * 32;
+    float4 *fez = fez_all + cw * 32;
     unsigned long long *best = best_all + cw * 32;
     float *flen = reinterpret_cast<float *>(smem + L.flen) + cw * 32;
     uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
@@ -433,11 +464,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         const int k0 = lane, k1 = 32 + lane;
         // plane of float k of a fiber: its address for fiber 0 of the warp and its stride in floats
         auto plane = [&](int k, int &stride) -> float * {
-            // fe = (x0, x20, y0, y20), fez = (z0, z20), fm = (x10, y10, z10, finite)
+            // fe = (x0, x20, y0, y20), fez = (z0, z20, h0, h20), fm = (x10, y10, z10, h10)
             const int pt = k / 3, c = k % 3;
             if (pt == 0 || pt == 20) {
                 if (c < 2) { stride = 4; return reinterpret_cast<float *>(fe) + 2 * c + (pt == 20 ? 1 : 0); }
-                stride = 2;
+                stride = 4;
                 return reinterpret_cast<float *>(fez) + (pt == 20 ? 1 : 0);
             }
             if (pt == 10) { stride = 4; return reinterpret_cast<float *>(fm) + c; }
@@ -467,7 +498,13 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         }
         fin = __reduce_and_sync(0xffffffffu, fin);   // bit j: every value of fiber j is finite
         __syncwarp();
-        fm[lane].w = (((fin >> lane) & 1u) && fjs >= 0) ? 1.f : 0.f;
+        {   // fm.w: NaN marks a non-finite fiber (or an empty slot); else the screen's half norms
+            const bool okf = ((fin >> lane) & 1u) && fjs >= 0;
+            const float4 e = fe[lane], m = fm[lane], z = fez[lane];
+            fm[lane].w = okf ? screen_half_norm(m.x, m.y, m.z) : __int_as_float(0x7fffffff);
+            fez[lane].z = okf ? screen_half_norm(e.x, e.z, z.x) : 0.f;
+            fez[lane].w = okf ? screen_half_norm(e.y, e.w, z.y) : 0.f;
+        }
         if (PAPER) {
             // chord length of this lane's fiber (reading R16), FP32, segments summed in order
             auto pt = [&](int i) -> float4 {
@@ -495,7 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     // evaluates that one candidate in full -- its fiber from shared memory, the centroid's 21 points from
     // the centroid-major copy -- with k_classify's arithmetic, and starts from its key.  It is one of the
     // candidates the tile stream would evaluate, so the result cannot change; a good start prunes the rest.
-    if (consumer && p.seed_code && inrange && fm[lane].w != 0.f) {
+    if (consumer && p.seed_code && inrange && !isnan(fm[lane].w)) {
         const int code = __ldg(p.seed_code + fidx);
         if (code >= 0) {
             const int tn = code >> 6, c = (code >> 1) & 31;
@@ -503,7 +540,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             const float4 *cc = p.tiles_cm + ((size_t)tn * TILE + c) * NPTS;
             const TileHdr *h = reinterpret_cast<const TileHdr *>(p.tiles + (size_t)tn * TILE_STRIDE_F4);
             const float4 E = fe[lane], F10 = fm[lane];
-            const float2 Ez = fez[lane];
+            const float4 Ez = fez[lane];
             if (PAPER) {
                 // paper mode: the orientation the end points infer, decided as in the dense loop (R17)
                 const float4 c0p = __ldg(cc), c20p = __ldg(cc + NPTS - 1);
@@ -562,8 +599,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         // ---- consumers ----
         const uint32_t lt_mask = (1u << lane) - 1u;
         const float4 myE = fe[lane], myF10 = fm[lane];
-        const float2 myEz = fez[lane];
-        const bool myok = myF10.w != 0.f;
+        const float2 myEz = make_float2(fez[lane].x, fez[lane].y);
+        const bool myok = !isnan(myF10.w);
         // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
         // starting from its 3-point running max r
         // excl: the round's entries are distinct fibers (a winners' round: at most one winner per
@@ -575,12 +612,23 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
 #endif
             if (lane < n) {
                 const uint32_t e = (uint32_t)qe[lane];
-                float r = qr[lane];
                 const int fl = (e >> 5) & 31, c = e & 31, o = (e >> 10) & 1, es = (e >> 11) & 3;
                 SEG_DCHECK(es < STAGES && (e >> 13) == 0);
                 // the candidate's tile: the ring stage recorded in its entry
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
+                float r;
+                if (PAPER) {
+                    r = qr[lane];
+                } else {
+                    // exact mode screened with estimates: the 3-point running max, exactly as the
+                    // dense test2 of the d2 form computes it (d2 and d2_pair_b agree bit for bit)
+                    const float4 a10 = fm[fl], E = fe[fl], Ez = fez[fl];
+                    const float4 *cq = T + c;
+                    r = fmaxf(fmaxf(d2(a10.x, a10.y, a10.z, cq[10 * TILE]),
+                                    d2(E.x, E.z, Ez.x, cq[o ? 20 * TILE : 0])),
+                              d2(E.y, E.w, Ez.y, cq[o ? 0 : 20 * TILE]));
+                }
                 const float thr2 = reinterpret_cast<const TileHdr *>(estage)->thr2;
                 const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
@@ -665,6 +713,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             long long ts0 = 0;
             if (STATS) ts0 = clock64();
             const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
+            const float tcmp = (PAPER || SCREEN_OFF) ? tau : __fmul_rn(tau, 0.5f);   // exact mode screens at half scale
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
             const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sqrtf(tau) + CULL_EPS);
             uint32_t pm = __ballot_sync(0xffffffffu, pass);
@@ -687,6 +736,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                 const float4 c0 = T[lane], c20 = T[20 * TILE + lane];
                 while (pm) {
                     // FB fibers per step: independent chains (ILP) and one warp vote per step
+                    constexpr int FB = PAPER ? SEG_FB_PAPER : SEG_FB;
                     int jj[FB];
                     float rdv[FB], riv[FB], tjv[FB];
                     uint32_t hit = 0;
@@ -708,13 +758,26 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const int j = jj[q];
                         // fiber j's end points arrive packed: (x0, x20), (y0, y20), (z0, z20)
                         const float4 E = fe[j];
-                        const float2 Ez = fez[j];
+                        const float4 Ez = fez[j];
                         const float4 a10 = fm[j];
-                        const float tj = __shfl_sync(0xffffffffu, tau, j);
-                        const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)), EZ = f2u(Ez);
-                        const float m10 = d2(a10.x, a10.y, a10.z, c10);                 // test1
-                        const float2 R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);      // (e0,0, e20,0)
-                        const float2 R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);  // (e0,20, e20,20)
+                        const float tj = __shfl_sync(0xffffffffu, tcmp, j);
+                        const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)),
+                                  EZ = f2u(make_float2(Ez.x, Ez.y));
+                        float m10;
+                        float2 R0, R20;
+                        if (PAPER || SCREEN_OFF) {
+                            m10 = d2(a10.x, a10.y, a10.z, c10);                         // test1
+                            R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);               // (e0,0, e20,0)
+                            R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);           // (e0,20, e20,20)
+                        } else {
+                            // exact mode: the dot-product screen, half scale (never above d2 / 2; the
+                            // candidate rounds re-evaluate the three points exactly)
+                            m10 = __fmaf_rn(a10.x, -c10.x, __fmaf_rn(a10.y, -c10.y,
+                                      __fmaf_rn(a10.z, -c10.z, __fadd_rn(a10.w, c10.w))));
+                            const u64 EN = f2u(make_float2(Ez.z, Ez.w));
+                            R0 = screen_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z, add_pair_b(EN, c0.w));
+                            R20 = screen_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z, add_pair_b(EN, c20.w));
+                        }
                         rdv[q] = fmaxf(fmaxf(m10, R0.x), R20.y);                        // test2, direct
                         riv[q] = fmaxf(fmaxf(m10, R20.x), R0.y);                        // test2, inverse
                         if (PAPER) {
@@ -747,7 +810,8 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         const bool ad = rd <= tj, ai = ri <= tj;
                         // best-first: the centroid with the smallest 3-point score goes to the
                         // winners' round, every other surviving orientation to q2
-                        const float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
+                        float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
+                        if (!PAPER) sc = fmaxf(sc, 0.f);   // screen values may be < 0; keep the key order
                         // the lane rides in the score's 5 low mantissa bits: REDUX.MIN names the winner
                         // directly (a heuristic choice; every survivor is still evaluated)
                         const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
@@ -759,7 +823,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         SEG_DCHECK(np < PECAP && j >= 0 && j < 32);
                         if (win) {
                             pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
-                            pr[np] = sc;
+                            if (PAPER) pr[np] = sc;   // exact mode: the round re-evaluates the 3 points
                         }
                         ++np;
                         const bool qd = ad && !(win && wo == 0), qi = ai && !(win && wo == 1);
@@ -767,12 +831,12 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         if (qd) {
                             const int pos = n2 + __popc(bd & lt_mask);
                             q2e[pos] = (uint16_t)e;
-                            q2r[pos] = rd;
+                            if (PAPER) q2r[pos] = rd;
                         }
                         if (qi) {
                             const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
                             q2e[pos] = (uint16_t)(e | (1u << 10));
-                            q2r[pos] = ri;
+                            if (PAPER) q2r[pos] = ri;
                         }
                         n2 += __popc(bd) + __popc(bi);
                         SEG_DCHECK(n2 <= Q2CAP);
@@ -792,7 +856,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             const unsigned long long key = best[lane];
             int lab;
             float dd;
-            if (fm[lane].w == 0.f) {
+            if (isnan(fm[lane].w)) {
                 lab = -1;
                 dd = __int_as_float(0x7fffffff);  // NaN: non-finite fiber
             } else if (key != KEY_NONE) {
@@ -805,7 +869,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             if (p.keys) {
                 // row f4: the raw best key for an atlas-sharded run (all_reduce MIN over the shards);
                 // exchange space: every key < 2^63, NONE = INT64_MAX, non-finite = INT64_MAX - 1
-                p.keys[fidx] = fm[lane].w == 0.f ? KEY_X_NONFINITE : key == KEY_NONE ? KEY_X_NONE : key;
+                p.keys[fidx] = isnan(fm[lane].w) ? KEY_X_NONFINITE : key == KEY_NONE ? KEY_X_NONE : key;
             } else {
                 p.label[fidx] = lab;
                 p.dist[fidx] = dd;

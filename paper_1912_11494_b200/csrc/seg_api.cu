@@ -414,8 +414,12 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
             for (int i = 0; i < NPTS; ++i) {
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
-                tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] =
-                    make_float4(c[0], c[1], c[2], i == 0 ? clen[(size_t)m] : 0.f);
+                // w: paper mode -- point 0 carries the chord length (Eq. 3); exact mode -- points 0, 10, 20
+                // carry the lowered half squared norm of k_classify's dot-product screen (seg_internal.cuh)
+                const bool paper = (flags & SEG_MODE_PAPER) != 0;
+                const float w = paper ? (i == 0 ? clen[(size_t)m] : 0.f)
+                                      : (i == 0 || i == 10 || i == 20) ? screen_half_norm_host(c) : 0.f;
+                tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] = make_float4(c[0], c[1], c[2], w);
                 tiles_cm[((size_t)t * TILE + k) * NPTS + i] = make_float4(c[0], c[1], c[2], 0.f);
                 for (int d = 0; d < 3; ++d) {
                     lo[d] = std::min(lo[d], c[d]);

@@ -1,6 +1,7 @@
 // seg_internal.cuh -- device data layout shared by the C-ABI layer (seg_api.cu) and the
 // sm_100a kernels (classify.cu).  Product code only; the oracle never includes it.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -22,6 +23,27 @@ constexpr int TILE_HDR_F4 = 7;           // the tile's 112-B TileHdr travels in 
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
 constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,816 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
+
+// Exact mode's dot-product screen for test1 / test2.  Each squared distance of the
+// dense loop is estimated as h = (|a|^2/2)' + (|c|^2/2)' - a.c (one FADD + three FFMA, against three
+// FADD + FMUL + two FFMA for d2), where (|x|^2/2)' = |x|^2/2 * (1 - 2^-18) - 2^-62 rounded down: the
+// lowered half norms.  Bound: the four roundings of h cost at most 4u(|a|^2 + |c|^2), the kernel's own
+// d2 differs from the true value by at most 8u(|a|^2 + |c|^2) (u = 2^-24, |a - c|^2 <= 2(|a|^2 + |c|^2)),
+// and the fiber's half norm is computed in FP32 with at most 5u of its own error; the 2^-18 = 64u
+// lowering exceeds their sum, and 2^-62 covers subnormal roundings.  So h <= d2/2 for every pair:
+// "h <= tau/2" keeps every pair "d2 <= tau" keeps (a superset; the candidate rounds then evaluate
+// exactly, from d2).  A point with a coordinate beyond 2^50 gets -inf (its products stay exact inside
+// the FMA, so h = -inf: always kept) -- no overflow is possible below that.
+constexpr float SCREEN_SAFE = 0x1p50f;
+inline float screen_half_norm_host(const float *c) {
+    if (!(std::fabs(c[0]) <= SCREEN_SAFE && std::fabs(c[1]) <= SCREEN_SAFE && std::fabs(c[2]) <= SCREEN_SAFE))
+        return -INFINITY;
+    const double n = (double)c[0] * c[0] + (double)c[1] * c[1] + (double)c[2] * c[2];
+    const double v = 0.5 * n * (1.0 - 0x1p-18) - 0x1p-62;
+    float f = (float)v;
+    while ((double)f > v) f = std::nextafter(f, -INFINITY);
+    return f;
+}
 constexpr int MORTON_BITS = 6;           // per axis, the grid seg_create scales (inv_cell) for
 constexpr int MORTON_BUCKETS = 1 << (3 * MORTON_BITS);
 // the prepass grid per call: 7 bits per axis (2^21 buckets) from this many fibers on, else 6 (2^18):

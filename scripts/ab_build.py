@@ -1,5 +1,5 @@
 """A/B timing of library builds with extra nvcc defines: python scripts/ab_build.py CFG "-DX" "-DY" ...
-(the empty string = production).  Prints the per-kernel event times from seg_profile_read."""
+(the empty string = production).  AB_MODE=paper: paper-semantics atlases.  Prints the per-kernel event times from seg_profile_read."""
 import ctypes, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -22,11 +22,13 @@ for k, d in enumerate(defs):
     L = ctypes.CDLL(out)
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     L.seg_create.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.POINTER(vp)]
+    L.seg_create_ex.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(vp)]
     L.seg_classify.argtypes = [vp, vp, i64, vp, vp, vp]
     L.seg_profile_enable.argtypes = [vp, i32]
     L.seg_profile_read.argtypes = [vp, vp, vp, vp, i32, ctypes.POINTER(i32)]
     h = vp()
-    assert L.seg_create(c.data_ptr(), b.data_ptr(), at.M, t.data_ptr(), at.B, -1, ctypes.byref(h)) == 0
+    flags = 1 if os.environ.get("AB_MODE") == "paper" else 0   # SEG_MODE_PAPER
+    assert L.seg_create_ex(c.data_ptr(), b.data_ptr(), at.M, t.data_ptr(), at.B, -1, flags, ctypes.byref(h)) == 0
     lab = torch.empty(N, dtype=torch.int32, device="cuda"); dd = torch.empty(N, dtype=torch.float32, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
