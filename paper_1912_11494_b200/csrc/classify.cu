@@ -290,7 +290,10 @@ size_t morton_scratch_words(int bits) {
 //   a8  epilogue: label / sqrt(d^2) (paper mode: the score) stored through the permutation, or the
 //       raw key for an atlas-sharded run (row f4).
 // ----------------------------------------------------------------------------------------
-constexpr int NCW = 8;                 // consumer warps (4 warps x 3 CTAs/SM measured slower: 8.74 vs 7.73 ms)
+#ifndef SEG_NCW
+#define SEG_NCW 8
+#endif
+constexpr int NCW = SEG_NCW;           // consumer warps (4 warps x 3 CTAs/SM measured slower: 8.74 vs 7.73 ms)
 constexpr int CTAS_PER_SM = 2;
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
@@ -300,12 +303,12 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
 // the dot-product screen: 2 (cfg 3: 3 -> +1.3%, 4 -> +1.1%, 1 -> +5.4%; the screen's shorter chains
-// make the smaller step pay).  Paper mode, d2 form: 3 (the d2 form at 2: +0.4%, at 4: +0.8%).
+// make the smaller step pay).  Paper mode, d2 form, with the per-fiber VOTE: 2 as well (3: +2.1%).
 #ifndef SEG_FB
 #define SEG_FB 2
 #endif
 #ifndef SEG_FB_PAPER
-#define SEG_FB_PAPER 3
+#define SEG_FB_PAPER 2
 #endif
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
@@ -788,10 +791,11 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                             else riv[q] = INFINITY;
                         }
                         tjv[q] = tj;
-                        if (jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj) hit |= 1u << q;
+                        // one VOTE.ANY per fiber: far shorter latency than a REDUX.OR of the step's bits
+                        // (cfg 3: -3.6%)
+                        if (__any_sync(0xffffffffu, jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
-                    hit = __reduce_or_sync(0xffffffffu, hit);
 #if defined(SEG_EXP) && SEG_EXP == 3
                     hit = p.n < 0 ? hit : 0;  // experiment: dense test1+test2 only (opaque, so it is not dead code)
 #endif
