@@ -718,7 +718,12 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
             const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
             const float tcmp = (PAPER || SCREEN_OFF) ? tau : __fmul_rn(tau, 0.5f);   // exact mode screens at half scale
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
-            const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sqrtf(tau) + CULL_EPS);
+            // MUFU.SQRT (relative error < 2^-22) raised by 2^-20 so the radius never falls below the
+            // exact one: no IEEE slow-path branch on the per-tile chain
+            float sq;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(tau));
+            const float sb = __fmaf_ru(sq, 1.f + 0x1p-20f, CULL_EPS);
+            const bool pass = myok && tile_may_pass(myE, myEz, myF10, th, sb);
             uint32_t pm = __ballot_sync(0xffffffffu, pass);
             if (STATS && lane == 0) cnt[ST_CYC_SPHERE] += clock64() - ts0;
 #if defined(SEG_EXP) && SEG_EXP == 1
