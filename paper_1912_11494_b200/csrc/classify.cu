@@ -301,6 +301,14 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 #define SEG_STAGES 3
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
+#ifndef SEG_CULL_UNROLL
+#define SEG_CULL_UNROLL 32
+#endif
+#ifndef SEG_DENSE_UNROLL
+#define SEG_DENSE_UNROLL 1
+#endif
+constexpr int CULL_UNROLL = SEG_CULL_UNROLL;     // k_cull's 32-tile chunk loop
+constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
 // the dot-product screen: 2 (cfg 3: 3 -> +1.3%, 4 -> +1.1%, 1 -> +5.4%; the screen's shorter chains
 // make the smaller step pay).  Paper mode, d2 form, with the per-fiber VOTE: 2 as well (3: +2.1%).
@@ -742,6 +750,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                 // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
                 const float4 c10 = T[10 * TILE + lane];
                 const float4 c0 = T[lane], c20 = T[20 * TILE + lane];
+#pragma unroll DENSE_UNROLL
                 while (pm) {
                     // FB fibers per step: independent chains (ILP) and one warp vote per step
                     constexpr int FB = PAPER ? SEG_FB_PAPER : SEG_FB;
@@ -967,7 +976,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
                 // 32 tiles per chunk: independent header loads and tests (ILP)
                 const int nt = min(32, h.t1 - t0);
                 uint32_t pm = 0, cm = 0;
-#pragma unroll 4
+#pragma unroll CULL_UNROLL
                 for (int j = 0; j < 32; ++j) {
                     if (j < nt) {
                         const CullTile ct = p.ct[t0 + j];
