@@ -307,6 +307,14 @@ constexpr int STAGES = SEG_STAGES;     // tile ring depth
 #ifndef SEG_DENSE_UNROLL
 #define SEG_DENSE_UNROLL 1
 #endif
+#ifndef SEG_INGEST_UNROLL
+#define SEG_INGEST_UNROLL 32
+#endif
+#ifndef SEG_BUNDLE_UNROLL
+#define SEG_BUNDLE_UNROLL 32
+#endif
+constexpr int INGEST_UNROLL = SEG_INGEST_UNROLL; // k_classify's fiber ingest loops (32 fibers per warp)
+constexpr int BUNDLE_UNROLL = SEG_BUNDLE_UNROLL; // k_cull's 32-bundle sphere loop
 constexpr int CULL_UNROLL = SEG_CULL_UNROLL;     // k_cull's 32-tile chunk loop
 constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         int s0 = 1, s1 = 1;
         float *d0 = plane(k0, s0), *d1 = plane(k1 < 3 * NPTS ? k1 : 0, s1);
         int fjs = -1;
-#pragma unroll 8
+#pragma unroll INGEST_UNROLL
         for (int j = 0; j < 32; ++j) {
             const int fj = __shfl_sync(0xffffffffu, fidx, j);
             if (lane == j) fjs = fj;
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         }
         cp_async_wait_all();
         uint32_t fin = 0;   // bit j: this lane's two values of fiber j are finite
-#pragma unroll 8
+#pragma unroll INGEST_UNROLL
         for (int j = 0; j < 32; ++j) {
             const bool ok = isfinite(d0[j * s0]) && (k1 >= 3 * NPTS || isfinite(d1[j * s1]));
             fin |= (ok ? 1u : 0u) << j;
@@ -954,7 +962,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
     // bundles some fiber of the CTA may need (point-10 sphere + threshold, exact)
     for (int b0 = 0; b0 < p.B; b0 += 32) {
         uint32_t m = 0;
-#pragma unroll 8
+#pragma unroll BUNDLE_UNROLL
         for (int j = 0; j < 32; ++j) {
             const float4 c = stage_bh ? sbs[b0 + j] : bsphere(b0 + j);
             m |= (d2(F10.x, F10.y, F10.z, c) <= c.w ? 1u : 0u) << j;
