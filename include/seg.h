@@ -108,8 +108,8 @@ int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M,
  *   stream, of the GPU count and of the order of centroids in seg_create.
  *   Scratch is stream-ordered, from a memory pool the atlas owns (cached between calls, released by
  *   seg_destroy; the device's default pool is not touched).  fibers needs 4-byte alignment.
- *   Device-resident inputs run in slices of at most 2^23 fibers (bounded scratch: 8 B per fiber
- *   plus 2 (T + 2) B per 256 fibers); fibers are independent, so the slicing changes no result.
+ *   Device-resident inputs run in slices of at most 2^23 fibers (bounded scratch: 16 B per fiber --
+ *   Morton key, bucket rank, permutation, seed code -- plus 2 (T + 2) B per 256 fibers); fibers are independent, so the slicing changes no result.
  *   N = 0 is a no-op returning SEG_OK.
  * Errors: SEG_EINVAL (null atlas, null pointer with N > 0, N > 2^31 - 1, mixed host
  * and device pointers, a device pointer on another device, misalignment),

@@ -176,7 +176,7 @@ __global__ void k_morton_hist(MortonParams p) {
         const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * (p.inv_cell.z * sc), 0.f), lim);
         const uint32_t k = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
         p.key[i] = k;
-        atomicAdd(p.hist + k, 1u);
+        p.rank[i] = atomicAdd(p.hist + k, 1u);   // the rank in the bucket: the scatter needs no atomic
     }
 }
 
@@ -242,7 +242,7 @@ __global__ void k_morton_scatter(MortonParams p) {
     if (i >= p.n) return;
     const uint32_t k = p.key[i];
     SEG_DCHECK(k < (1u << (3 * p.bits)));
-    const uint32_t pos = atomicAdd(p.hist + k, 1u) + __ldg(p.bsum + k / SCAN_B);
+    const uint32_t pos = __ldg(p.hist + k) + p.rank[i] + __ldg(p.bsum + k / SCAN_B);
     SEG_DCHECK(pos < (uint32_t)p.n);
     p.perm[pos] = i;
 }

@@ -602,6 +602,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
         const int bits = morton_bits_for(n);
         SEG_CUDA(sc.get(&hist, sizeof(uint32_t) * morton_scratch_words(bits)), "seg_classify: scratch allocation");
         MortonParams mp{fib, n, a->lo, a->inv_cell, key, hist, hist + ((size_t)1 << (3 * bits)), perm, bits};
+        SEG_CUDA(sc.get(&mp.rank, sizeof(uint32_t) * (size_t)n), "seg_classify: scratch allocation");
         SEG_CUDA(launch_morton_prepass(mp, s), "seg_classify: prepass launch");
     }
     uint32_t *tbits = nullptr;
@@ -623,8 +624,8 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
 }
 
 // Device inputs are classified in slices of at most DEV_CHUNK fibers.  Fibers are independent, so the
-// result does not depend on the slicing; it bounds the per-call scratch (Morton keys and permutation,
-// 8 B per fiber; the per-CTA tile lists, (T + 2) x 2 B per 256 fibers) whatever N is.  Configurations
+// result does not depend on the slicing; it bounds the per-call scratch (Morton keys, bucket ranks,
+// permutation and seed codes, 16 B per fiber; the per-CTA tile lists, (T + 2) x 2 B per 256 fibers) whatever N is.  Configurations
 // up to 8.4 M fibers run as one slice.
 constexpr int64_t DEV_CHUNK = int64_t(1) << 23;
 int classify_device_sliced(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab, float *dist,

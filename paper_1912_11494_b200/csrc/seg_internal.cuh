@@ -113,6 +113,7 @@ struct MortonParams {
     uint32_t *bsum;           // [MORTON_BUCKETS / 1024] per-block totals, then offsets
     int32_t *perm;            // [n]
     int bits;                 // grid bits per axis for this call (morton_bits_for(n))
+    uint32_t *rank = nullptr; // [n] each fiber's arrival rank in its bucket (k_morton_hist's atomic)
 };
 
 // Row f3 (group.cu): the stable partition of the fibers by label.
