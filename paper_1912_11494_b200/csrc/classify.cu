@@ -152,7 +152,10 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // up to 10 bits -> e
     return v;
 }
 
-constexpr int MORTON_FPT = 4;   // fibers per thread in k_morton_hist (independent loads in flight)
+#ifndef SEG_MORTON_FPT
+#define SEG_MORTON_FPT 8
+#endif
+constexpr int MORTON_FPT = SEG_MORTON_FPT;   // fibers per thread in k_morton_hist (independent loads in flight)
 
 __global__ void k_morton_hist(MortonParams p) {
     const float lim = (float)((1 << p.bits) - 1);
@@ -316,6 +319,10 @@ constexpr int STAGES = SEG_STAGES;     // tile ring depth
 constexpr int INGEST_UNROLL = SEG_INGEST_UNROLL; // k_classify's fiber ingest loops (32 fibers per warp)
 constexpr int BUNDLE_UNROLL = SEG_BUNDLE_UNROLL; // k_cull's 32-bundle sphere loop
 constexpr int CULL_UNROLL = SEG_CULL_UNROLL;     // k_cull's 32-tile chunk loop
+#ifndef SEG_RANK_UNROLL
+#define SEG_RANK_UNROLL 4
+#endif
+constexpr int RANK_UNROLL = SEG_RANK_UNROLL;     // k_cull's best-first ranking loop
 constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
 // the dot-product screen: 2 (cfg 3: 3 -> +1.3%, 4 -> +1.1%, 1 -> +5.4%; the screen's shorter chains
@@ -1102,6 +1109,7 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
         const int ti = lst[i];
         const uint32_t ki = prio[ti];
         int rank = 0;
+#pragma unroll RANK_UNROLL
         for (int k = 0; k < n; ++k) {
             const int tk = lst[k];
             const uint32_t kk = prio[tk];
