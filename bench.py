@@ -246,7 +246,9 @@ def main():
     value = pairs / (ms_step * 1e-3)
     fibers_per_s = N * world / (ms_step * 1e-3)
     clocks = clk.summary()
-    launches_per_step = 6 if N >= 4096 else 2           # hist, scan_blocks, scan_totals, scatter, cull, classify
+    # hist, scan_blocks, scan_totals, scatter (N >= 4096), cull, cta_order (grids of <= 64 waves), classify
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    launches_per_step = (4 if N >= 4096 else 0) + 2 + (1 if -(-N // 256) <= 64 * 2 * sms else 0)
     res_lab = lab.cpu().numpy()
 
     # ---------------- stage counters + roofline of the dominant kernel ----------------

@@ -446,6 +446,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool consumer = warp < NCW;
+    // the fiber window (and k_cull's list) this CTA works on: the longest lists launch first
+    const int cta = p.cta_order ? __ldg(p.cta_order + blockIdx.x) : (int)blockIdx.x;
+    SEG_DCHECK(cta >= 0 && (size_t)cta * FPC < (size_t)p.n);
     const int cw = consumer ? warp : 0;
     float2 *fxy = reinterpret_cast<float2 *>(smem + L.fxy) + cw * (NMID * 32);   // [18][32]
     float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NMID * 32);       // [18][32]
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     // the CTA's fibers interleaved over the warps (fiber i -> warp i % NCW): every warp gets a similar
     // share of every tile's work, so the warps sharing the ring stay in step (cfg 3: -1%, cfg 1: -6%
     // against contiguous 32-fiber slices; the CTA's fibers are all Morton-close anyway)
-    const int gi = blockIdx.x * FPC + lane * NCW + warp;
+    const int gi = cta * FPC + lane * NCW + warp;
     const bool inrange = consumer && gi < p.n;
     const int fidx = inrange ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
     SEG_DCHECK(!inrange || (fidx >= 0 && fidx < p.n));
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
         if (lane == 0) {
             const unsigned short *lst_g =
-                reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)blockIdx.x * cull_stride(p.T);
+                reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)cta * cull_stride(p.T);
             const int nlist = __ldg(lst_g);
             SEG_DCHECK(nlist >= 0 && nlist <= p.T);
             int k = 0;
@@ -1104,7 +1107,10 @@ __global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
     // the running best tight early, which prunes the later tiles.
     const int n = nlist;
     uint16_t *out = reinterpret_cast<uint16_t *>(p.tile_bits) + (size_t)blockIdx.x * cull_stride(p.T);
-    if (threadIdx.x == 0) out[0] = (uint16_t)n;
+    if (threadIdx.x == 0) {
+        out[0] = (uint16_t)n;
+        if (p.cta_order) p.cta_order[blockIdx.x] = n;   // k_cta_order's input (LPT launch order)
+    }
     for (int i = threadIdx.x; i < n; i += FPC) {
         const int ti = lst[i];
         const uint32_t ki = prio[ti];
@@ -1153,6 +1159,66 @@ int classify_max_tiles() { return MAX_TILES; }
 
 size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(cull_stride(T) / 2); }
 
+// Longest-processing-time-first launch order for k_classify: CTAs sorted by the length of k_cull's tile
+// list (descending, in 2,048 buckets), so the longest windows do not land in the grid's last wave.  Any
+// order gives the same results (windows are independent).
+constexpr int LPT_BUCKETS = 2048;
+// k_cull left each window's list length in order[window]; one block reads them all (coalesced, at most
+// 32 per thread: slices hold at most 2^23 fibers = 32,768 windows), then overwrites order with the ranking.
+constexpr int LPT_PER_THREAD = 32;
+__global__ void __launch_bounds__(1024) k_cta_order(int ncta, int T, int32_t *order) {
+    __shared__ uint32_t cnt[LPT_BUCKETS];
+    __shared__ uint32_t wsum[33];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    for (int i = t; i < LPT_BUCKETS; i += 1024) cnt[i] = 0;
+    __syncthreads();
+    SEG_DCHECK(ncta <= 1024 * LPT_PER_THREAD);
+    int bk[LPT_PER_THREAD];
+#pragma unroll
+    for (int k = 0; k < LPT_PER_THREAD; ++k) {
+        const int c = t + 1024 * k;
+        const long long len = c < ncta ? order[c] : 0;
+        bk[k] = LPT_BUCKETS - 1 - (int)min((long long)LPT_BUCKETS - 1, len * LPT_BUCKETS / (T + 1));
+    }
+#pragma unroll
+    for (int k = 0; k < LPT_PER_THREAD; ++k)
+        if (t + 1024 * k < ncta) atomicAdd(&cnt[bk[k]], 1u);
+    __syncthreads();
+    const uint32_t a = cnt[2 * t], b = cnt[2 * t + 1];
+    uint32_t incl = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = wsum[lane];
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += v;
+        }
+        wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint32_t ex = wsum[w] + incl - (a + b);
+    cnt[2 * t] = ex;
+    cnt[2 * t + 1] = ex + a;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < LPT_PER_THREAD; ++k) {
+        const int c = t + 1024 * k;
+        if (c < ncta) {
+            const uint32_t pos = atomicAdd(&cnt[bk[k]], 1u);
+            SEG_DCHECK(pos < (uint32_t)ncta);
+            order[pos] = c;
+        }
+    }
+}
+
 cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s, cudaEvent_t after_cull) {
     if (p.n <= 0) return cudaSuccess;
     const size_t smem = classify_smem_bytes(p.B, p.T);
@@ -1163,6 +1229,7 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
     cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
     if (e != cudaSuccess) return e;
     k_cull<<<grid, FPC, cull_smem, s>>>(p);
+    if (p.cta_order) k_cta_order<<<1, 1024, 0, s>>>(grid, p.T, p.cta_order);
     if (after_cull) {
         e = cudaEventRecord(after_cull, s);
         if (e != cudaSuccess) return e;

@@ -48,6 +48,7 @@ struct seg_atlas {
     int64_t M = 0;
     int B = 0, T = 0;
     int paper = 0;                // SEG_MODE_PAPER: score = d_ME (inferred orientation) + TN
+    int sms = 148;                // SM count of the device (k_classify's launch-order heuristic)
     float4 *tiles = nullptr;      // [T][TILE_STRIDE_F4]: header + [21][32] points (point 0's w = chord length)
     float4 *tiles_cm = nullptr;   // [T][32][21] the same points centroid-major (the seed evaluation's loads)
     TileHdr *th = nullptr;        // [T]
@@ -481,6 +482,7 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
     if (!a) return fail(SEG_ENOMEM, "seg_create: host allocation failed");
     a->device = device;
     a->paper = (flags & SEG_MODE_PAPER) ? 1 : 0;
+    if (cudaDeviceGetAttribute(&a->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) a->sms = 148;
     a->M = M;
     a->B = B;
     a->T = P.T;
@@ -616,6 +618,14 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
 #endif
         SEG_CUDA(sc.get(&cp.seed_code, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
     }
+#ifndef SEG_NO_LPT
+    {   // longest-list-first launch order (k_cta_order) where the grid's last wave is a visible share:
+        // up to 64 waves of 2 CTAs per SM (cfg 1: -9%, cfg 3: -0.4%; cfg 4's 105 waves: +0.2% without it)
+        const int grid = (int)((n + classify_fibers_per_cta() - 1) / classify_fibers_per_cta());
+        if (grid <= 64 * 2 * a->sms)
+            SEG_CUDA(sc.get(&cp.cta_order, sizeof(int32_t) * (size_t)grid), "seg_classify: scratch allocation");
+    }
+#endif
     if (ev) SEG_CUDA(cudaEventRecord(ev[1], s), "seg_classify: profile event");
     cudaError_t e = launch_classify(cp, d_stats != nullptr, s, ev ? ev[2] : nullptr);
     if (ev && e == cudaSuccess) e = cudaEventRecord(ev[3], s);

@@ -101,6 +101,7 @@ struct ClassifyParams {
     unsigned long long *keys;  // nullable [n]: write the best keys (row f4) instead of label / dist
     int32_t *seed_code;            // nullable [n] by fiber: k_cull's seed candidate, (tile << 6) | (centroid << 1) | o, -1 = none
     const float4 *tiles_cm;        // [T][32][21] centroid-major copy of the tile points (the seed evaluation)
+    int32_t *cta_order = nullptr;  // nullable [grid]: k_classify's CTA i works on fiber window cta_order[i]
 };
 
 struct MortonParams {
