@@ -930,7 +930,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
 // best-first (see below).  A separate, light kernel (no big shared-memory ring) so its
 // latency-bound header loads run at full occupancy.
 // ----------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(FPC) k_cull(ClassifyParams p) {
+#ifndef SEG_CULL_MAXREG_CTAS
+#define SEG_CULL_MAXREG_CTAS 5
+#endif
+__global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyParams p) {
     // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list (u16)
     extern __shared__ uint32_t sbits[];
     const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
