@@ -1,11 +1,13 @@
 """CPU oracle for the segmentation hot path -- TEST INFRASTRUCTURE ONLY.
 
-Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
-reference legs may import this package.  It shares no code with
+Only tests/, __graft_entry__.smoke(), bench.py's cpu_baseline / --impl
+reference legs and scripts/oracle_full.py (which caches oracle outputs) may import
+this package.  It shares no code with
 paper_1912_11494_b200/ (the CUDA product path) and the product never imports it.
 
 oracle.c holds the arithmetic (plain definition of Eq. 1-2 and Alg. 1's
-closest-bundle labelling in double precision; see its header for citations).
+closest-bundle labelling in double precision, and the sound-discard variants that
+reach the same labels bitwise; see its header for citations).
 This module only compiles it with gcc, marshals numpy arrays through ctypes and
 splits a fiber batch into contiguous chunks over host threads (each thread
 writes only its own output slots, as PAPER.md:152 describes for the paper's own
@@ -55,12 +57,18 @@ def _load():
             lib.oracle_dme_d2.argtypes = [f32p, f32p]
             lib.oracle_dme.restype = ctypes.c_double
             lib.oracle_dme.argtypes = [f32p, f32p]
-            for fn in (lib.oracle_classify, lib.oracle_classify_paper):
+            cls_args = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                        ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            lib.oracle_classify.restype = ctypes.c_int
+            lib.oracle_classify.argtypes = cls_args + [ctypes.c_void_p]
+            lib.oracle_classify_paper.restype = ctypes.c_int
+            lib.oracle_classify_paper.argtypes = cls_args + [ctypes.c_void_p] * 3
+            for fn in (lib.oracle_classify_sound, lib.oracle_classify_paper_sound):
                 fn.restype = ctypes.c_int
-                fn.argtypes = [
-                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
-                    ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
-                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+                fn.argtypes = cls_args
+            lib.oracle_orientation_ambiguous.restype = ctypes.c_int
+            lib.oracle_orientation_ambiguous.argtypes = [f32p, f32p]
             lib.oracle_polyline_length.restype = ctypes.c_double
             lib.oracle_polyline_length.argtypes = [f32p]
             lib.oracle_tn.restype = ctypes.c_double
@@ -111,9 +119,15 @@ def tn(ls: float, lc: float) -> float:
 
 
 def endpoint_orientation(a, c) -> int:
-    """1 = inverse, 0 = direct: argmin of the end-point maxima, decided in FP32 (reading R17)."""
+    """1 = inverse, 0 = direct: argmin of the end-point maxima, ties -> direct, in double (reading R17)."""
     a, c = _f32(a).reshape(21, 3), _f32(c).reshape(21, 3)
     return int(_load().oracle_endpoint_orientation(_fp(a), _fp(c)))
+
+
+def orientation_ambiguous(a, c) -> bool:
+    """True iff the pair's orientation decision lies in the band of reading R20 (both orientations valid)."""
+    a, c = _f32(a).reshape(21, 3), _f32(c).reshape(21, 3)
+    return bool(_load().oracle_orientation_ambiguous(_fp(a), _fp(c)))
 
 
 def paper_score(a, c) -> float:
@@ -123,18 +137,25 @@ def paper_score(a, c) -> float:
 
 
 def classify(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM,
-             threads: int | None = None, want_d2b: bool = False, mode: str = "exact"):
-    """Plain-definition classification of fibers [n,21,3] against the atlas.
+             threads: int | None = None, want_d2b: bool = False, mode: str = "exact",
+             sound: bool = False, want_bands: bool = False):
+    """Classification of fibers [n,21,3] against the atlas.
 
     mode "exact": Eq. 2 d_ME (the north_star metric); mode "paper": the paper's complete metric
     d_ME in the end-point-inferred orientation + TN (Eq. 3), SURVEY.md Sec. 8(f) row f1.
-    Returns dict(label int32[n], dist float64[n], decidable bool[n][, d2b float64[n,B]]);
-    in paper mode d2b holds the per-bundle minimum *score* (mm), not a squared distance.
+    sound=False runs the plain definition (every pair, no discarding); sound=True the sound-discard
+    variant (Alg. 1's cascade cut at thr + 2 delta), bitwise the same label / dist / decidable.
+    Returns dict(label int32[n], dist float64[n], decidable bool[n]) plus, plain only:
+      want_d2b   -> d2b float64[n,B]: exact mode the per-bundle minimum of d_ME^2, paper mode the
+                    per-bundle minimum score S_b (mm);
+      want_bands -> lo, hi float64[n,B]: the per-bundle interval of correct values in mm (exact mode
+                    lo = hi = sqrt(d2b); paper mode [L_b, H_b] of reading R20).
     """
     if mode not in ("exact", "paper"):
         raise ValueError(f"unknown oracle mode {mode!r}")
+    if sound and (want_d2b or want_bands):
+        raise ValueError("the sound-discard variant does not produce per-bundle values")
     lib = _load()
-    fn = lib.oracle_classify if mode == "exact" else lib.oracle_classify_paper
     fib = _f32(fibers).reshape(-1, 21, 3)
     cen = _f32(centroids).reshape(-1, 21, 3)
     bid = np.ascontiguousarray(bundle_id, dtype=np.int32)
@@ -143,29 +164,47 @@ def classify(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM,
     label = np.empty(n, np.int32)
     dist = np.empty(n, np.float64)
     dec = np.empty(n, np.uint8)
-    d2b = np.empty((n, b), np.float64) if want_d2b else None
+    per_b = want_d2b or want_bands
+    d2b = np.empty((n, b), np.float64) if per_b else None
+    lo = np.empty((n, b), np.float64) if (want_bands and mode == "paper") else None
+    hi = np.empty((n, b), np.float64) if (want_bands and mode == "paper") else None
     if threads is None:
         threads = os.cpu_count() or 1
     threads = max(1, min(threads, n))
 
-    def run(lo, hi):
-        if hi <= lo:
-            return 0
-        return fn(
-            fib[lo:].ctypes.data, hi - lo, cen.ctypes.data, bid.ctypes.data, m,
-            thr.ctypes.data, b, float(delta),
-            label[lo:].ctypes.data, dist[lo:].ctypes.data, dec[lo:].ctypes.data,
-            d2b[lo:].ctypes.data if d2b is not None else None)
+    def ptr(a, lo_):
+        return a[lo_:].ctypes.data if a is not None else None
 
-    bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+    def run(lo_, hi_):
+        if hi_ <= lo_:
+            return 0
+        args = (fib[lo_:].ctypes.data, hi_ - lo_, cen.ctypes.data, bid.ctypes.data, m,
+                thr.ctypes.data, b, float(delta),
+                label[lo_:].ctypes.data, dist[lo_:].ctypes.data, dec[lo_:].ctypes.data)
+        if sound:
+            fn = lib.oracle_classify_sound if mode == "exact" else lib.oracle_classify_paper_sound
+            return fn(*args)
+        if mode == "exact":
+            return lib.oracle_classify(*args, ptr(d2b, lo_))
+        return lib.oracle_classify_paper(*args, ptr(d2b, lo_), ptr(lo, lo_), ptr(hi, lo_))
+
+    # more chunks than threads: fibers differ in cost (the sound variant), so small chunks balance
+    nchunk = threads if (threads == 1 or not sound) else min(n, threads * 16)
+    bounds = np.linspace(0, n, nchunk + 1).astype(np.int64)
     if threads == 1:
         rcs = [run(0, n)]
     else:
         with ThreadPoolExecutor(threads) as ex:
-            rcs = list(ex.map(lambda i: run(int(bounds[i]), int(bounds[i + 1])), range(threads)))
+            rcs = list(ex.map(lambda i: run(int(bounds[i]), int(bounds[i + 1])), range(nchunk)))
     if any(rcs):
         raise ValueError("oracle_classify: invalid arguments (bundle id out of range)")
     out = dict(label=label, dist=dist, decidable=dec.astype(bool))
-    if d2b is not None:
+    if want_d2b:
         out["d2b"] = d2b
+    if want_bands:
+        if mode == "exact":
+            out["lo"] = np.sqrt(d2b)
+            out["hi"] = out["lo"]
+        else:
+            out["lo"], out["hi"] = lo, hi
     return out

@@ -290,3 +290,83 @@ def test_paper_self_segmentation_and_monotonicity():
     hi = oracle.classify(fib, cen, bid, thr * np.float32(1.5), threads=1, mode="paper")
     assert np.all((lo["label"] < 0) | (hi["label"] >= 0))
     assert np.all(hi["dist"][lo["label"] >= 0] <= lo["dist"][lo["label"] >= 0] + 1e-12)
+
+
+# ----------------------------------------------------------------------------------
+# the paper-mode tie band (decidable flag; oracle/oracle.c label_paper, readings R17 + R20)
+# ----------------------------------------------------------------------------------
+def test_paper_tie_band_flag():
+    """decidable = False within 1e-3 mm of a threshold or of the runner-up bundle (scores with TN = 0:
+    translated copies have the fiber's own length), mirroring tests/test_oracle_pins.py's exact case."""
+    a = fiber_A()[None]
+    bid = np.array([0, 1], np.int32)
+    thr = np.array([4.0, 8.0], np.float32)
+
+    def run(t0, t1):
+        c = np.stack([fiber_A() + np.float32([t0, 0, 0]), fiber_A() + np.float32([0, t1, 0])])
+        return oracle.classify(a, c, bid, thr, mode="paper")
+
+    r = run(2.0, 6.0)
+    assert r["label"][0] == 0 and r["dist"][0] == 2.0 and r["decidable"][0]      # clear winner
+    r = run(4.0 - 2 ** -11, 6.0)                              # within 1e-3 of thr_0
+    assert r["label"][0] == 0 and not r["decidable"][0]
+    r = run(4.0 + 2 ** -11, 6.0)                              # just above thr_0, within band
+    assert r["label"][0] == 1 and not r["decidable"][0]
+    r = run(3.0, 3.0 + 2 ** -11)                              # runner-up within 1e-3
+    assert r["label"][0] == 0 and not r["decidable"][0]
+    assert run(3.0, 3.0 + 2 ** -8)["decidable"][0]            # runner-up 3.9e-3 away
+    r = run(9.0, 9.0)
+    assert r["label"][0] == -1 and r["decidable"][0]          # nothing within thr + delta
+
+
+def _loop_fiber():
+    """A closed, non-palindromic loop: a_0 = a_20 (so every centroid's end-point maxima tie exactly)."""
+    t = np.arange(21, dtype=np.float64) * (2 * np.pi / 20)
+    f = np.stack([8 * np.cos(t) - 8, 6 * np.sin(t), 2 * np.sin(2 * t)], 1)
+    return (np.round(f * 64) / 64).astype(np.float32)   # dyadic: translations stay exact in FP32
+
+
+def test_paper_orientation_band_makes_a_loop_undecidable():
+    """Reading R20: a_0 = a_20 ties the orientation decision exactly; the direct score (1, a translated
+    copy) and the inverse one differ, so either is a correct answer and the fiber is undecidable."""
+    a = _loop_fiber()
+    a[20] = a[0]
+    c = a + np.float32([0, 0, 1])
+    assert oracle.orientation_ambiguous(a, c) and oracle.endpoint_orientation(a, c) == 0
+    inv = oracle.max_pointwise(a, c, inverse=True)
+    assert inv > 5.0
+    r = oracle.classify(a[None], c[None], np.array([0], np.int32), np.array([4.0], np.float32), mode="paper",
+                        want_bands=True)
+    assert r["label"][0] == 0 and r["dist"][0] == pytest.approx(1.0, abs=1e-12)   # ties -> direct
+    assert not r["decidable"][0]
+    assert r["lo"][0, 0] == pytest.approx(1.0, abs=1e-12) and r["hi"][0, 0] == pytest.approx(inv, abs=1e-9)
+    # with a threshold no inverse score can reach, the label is still -1 or 0 depending on the choice:
+    # undecidable; with a palindromic fiber both orientations score alike and the fiber is decidable
+    p = np.zeros((21, 3), np.float32)
+    p[:, 0] = np.abs(np.arange(21, dtype=np.float32) - 10)
+    q = p + np.float32([0, 0, 1])
+    assert oracle.orientation_ambiguous(p, q)
+    r = oracle.classify(p[None], q[None], np.array([0], np.int32), np.array([4.0], np.float32), mode="paper")
+    assert r["label"][0] == 0 and r["dist"][0] == 1.0 and r["decidable"][0]
+
+
+def test_paper_orientation_band_edges():
+    """Just outside the band the orientation is a plain decision (decidable); just inside it is not."""
+    a = _loop_fiber()
+    a[20] = a[0] + np.float32([0.5, 0, 0])
+    c = a + np.float32([0, 0, 1])
+    # m_dir^2 = 1 (a translated copy); m_inv^2 = max(|a0 - c20|, |a20 - c0|)^2 = 0.25 + 1 = 1.25: direct
+    assert not oracle.orientation_ambiguous(a, c) and oracle.endpoint_orientation(a, c) == 0
+    r = oracle.classify(a[None], c[None], np.array([0], np.int32), np.array([40.0], np.float32), mode="paper")
+    assert r["label"][0] == 0 and r["decidable"][0] and r["dist"][0] == 1.0
+    # the band is 2^-18 relative on the squared maxima: an end-point offset e gives m_dir^2 = 1 and
+    # m_inv^2 = 1 + e^2, i.e. a relative gap e^2 -- inside for e = 2^-12 (2^-24), outside for 2^-8 (2^-16)
+    for e, inside in ((2.0 ** -12, True), (2.0 ** -8, False)):
+        a2 = _loop_fiber()
+        a2[20] = a2[0] + np.float32([e, 0, 0])
+        c2 = a2 + np.float32([0, 0, 1])
+        assert oracle.orientation_ambiguous(a2, c2) == inside and oracle.endpoint_orientation(a2, c2) == 0
+        r = oracle.classify(a2[None], c2[None], np.array([0], np.int32), np.array([40.0], np.float32),
+                            mode="paper")
+        assert r["label"][0] == 0 and r["dist"][0] == 1.0
+        assert r["decidable"][0] == (not inside)
