@@ -571,11 +571,14 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             const float4 E = fe[lane], F10 = fm[lane];
             const float4 Ez = fez[lane];
             if (PAPER) {
-                // paper mode: the orientation the end points infer, decided as in the dense loop (R17)
+                // paper mode: the orientation the end points infer, decided as in the dense loop (R17; an
+                // exact tie -> the caller's direct orientation, i.e. stored-inverse for a reversed centroid)
                 const float4 c0p = __ldg(cc), c20p = __ldg(cc + NPTS - 1);
                 const float e00 = d2(E.x, E.z, Ez.x, c0p), e2020 = d2(E.y, E.w, Ez.y, c20p);
                 const float e020 = d2(E.x, E.z, Ez.x, c20p), e200 = d2(E.y, E.w, Ez.y, c0p);
-                o = fmaxf(e020, e200) < fmaxf(e00, e2020) ? 1 : 0;
+                const float flip = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + 20 * TILE + c).w;
+                const float mi = fmaxf(e020, e200), md = fmaxf(e00, e2020);
+                o = (mi < md || (mi == md && flip != 0.f)) ? 1 : 0;
             }
             float r = d2(F10.x, F10.y, F10.z, __ldg(cc + 10));
             r = fmaxf(r, d2(E.x, E.z, Ez.x, __ldg(cc + (o ? NPTS - 1 : 0))));
@@ -590,7 +593,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 // score = d_ME + TN (Eq. 3), the lengths as the candidate rounds take them
                 const float clen = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + c).w;
                 const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[lane], clen));
-                if (sc <= __ldg(&h->thr)) {
+                // the same acceptance as a candidate of the tile stream: r <= thr2, then score <= thr
+                if (r <= __ldg(&h->thr2) && sc <= __ldg(&h->thr)) {
                     const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)__ldg(&h->bundle);
                     if (kk < best[lane]) best[lane] = kk;
                 }
@@ -817,9 +821,11 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         riv[q] = fmaxf(fmaxf(m10, R20.x), R0.y);                        // test2, inverse
                         if (PAPER) {
                             // the paper infers the direction from the end points:
-                            // argmin of the end-point maxima, ties -> direct (reading R17); only that
+                            // argmin of the end-point maxima, ties -> the caller's direct orientation
+                            // (reading R17; c20.w = 1 marks a centroid stored reversed); only that
                             // orientation goes on
-                            if (fmaxf(R20.x, R0.y) < fmaxf(R0.x, R20.y)) rdv[q] = INFINITY;
+                            const float mi = fmaxf(R20.x, R0.y), md = fmaxf(R0.x, R20.y);
+                            if (mi < md || (mi == md && c20.w != 0.f)) rdv[q] = INFINITY;
                             else riv[q] = INFINITY;
                         }
                         tjv[q] = tj;
@@ -847,13 +853,15 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
                         // best-first: the centroid with the smallest 3-point score goes to the
                         // winners' round, every other surviving orientation to q2
                         float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
+                        // the winner's orientation, chosen before the clamp below (a clamped negative
+                        // screen value would no longer compare equal to rd)
+                        const int wo = (ad && (!ai || rd <= ri)) ? 0 : 1;
                         if (!PAPER) sc = fmaxf(sc, 0.f);   // screen values may be < 0; keep the key order
                         // the lane rides in the score's 5 low mantissa bits: REDUX.MIN names the winner
                         // directly (a heuristic choice; every survivor is still evaluated)
                         const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
                         const int wl = (int)(smin & 31u);
                         const bool win = lane == wl;
-                        const int wo = (ad && rd == sc) ? 0 : 1;
                         if (STATS && lane == 0) cnt[ST_HITS]++;
                         const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
                         SEG_DCHECK(np < PECAP && j >= 0 && j < 32);

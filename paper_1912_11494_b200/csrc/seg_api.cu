@@ -415,10 +415,12 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
             for (int i = 0; i < NPTS; ++i) {
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
-                // w: paper mode -- point 0 carries the chord length (Eq. 3); exact mode -- points 0, 10, 20
-                // carry the lowered half squared norm of k_classify's dot-product screen (seg_internal.cuh)
+                // w: paper mode -- point 0 carries the chord length (Eq. 3), point 20 a 1 when the centroid is
+                // stored reversed (an exact end-point tie then picks the caller's direct orientation, so the
+                // result does not depend on the stored order); exact mode -- points 0, 10, 20 carry the
+                // lowered half squared norm of k_classify's dot-product screen (seg_internal.cuh)
                 const bool paper = (flags & SEG_MODE_PAPER) != 0;
-                const float w = paper ? (i == 0 ? clen[(size_t)m] : 0.f)
+                const float w = paper ? (i == 0 ? clen[(size_t)m] : i == 20 ? (P.flipped[m] ? 1.f : 0.f) : 0.f)
                                       : (i == 0 || i == 10 || i == 20) ? screen_half_norm_host(c) : 0.f;
                 tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] = make_float4(c[0], c[1], c[2], w);
                 tiles_cm[((size_t)t * TILE + k) * NPTS + i] = make_float4(c[0], c[1], c[2], 0.f);
@@ -776,8 +778,11 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
         const size_t bytes = sizeof(unsigned long long) * SEG_NSTATS;
         SEG_CUDA(a->pool ? cudaMallocFromPoolAsync((void **)&d_stats, bytes, a->pool, s) : cudaMallocAsync((void **)&d_stats, bytes, s),
                  "seg_classify_stats: scratch allocation");
-        SEG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * SEG_NSTATS, s),
-                 "seg_classify_stats: memset");
+        const cudaError_t em = cudaMemsetAsync(d_stats, 0, bytes, s);
+        if (em != cudaSuccess) {
+            cudaFreeAsync(d_stats, s);   // freed on every path
+            return cuda_fail(em, "seg_classify_stats: memset");
+        }
     }
     int rc = classify_device_sliced(a, fibers, N, label, dist, s, d_stats,
                                     reinterpret_cast<const unsigned long long *>(seed));
@@ -787,7 +792,9 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         cudaFreeAsync(d_stats, s);
         if (!rc && e != cudaSuccess) return cuda_fail(e, "seg_classify_stats: readback");
-        for (int k = 0; k < SEG_NSTATS; ++k) stats[k] += h[k];
+        // the counters are added only when both the classification and the readback succeeded
+        if (!rc && e == cudaSuccess)
+            for (int k = 0; k < SEG_NSTATS; ++k) stats[k] += h[k];
     }
     if (!rc) g_err.clear();
     return rc;

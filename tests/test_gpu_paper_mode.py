@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import oracle
-from parity_util import check_parity
+from parity_util import check_parity, check_parity_full
 from seg_testutil import fiber_A
 from synth import atlas_for_config, fibers_for_config, sample_indices
 
@@ -49,7 +49,7 @@ def test_paper_cfg0_full_parity(cfg0p):
     fib = fibers_for_config(0)
     lab, d = _gpu(A, fib)
     ref = oracle.classify(fib, at.centroids, at.bundle_id, at.thresh, mode="paper")
-    info = check_parity(lab, d, ref, "cfg0 paper")
+    info = check_parity_full(lab, d, fib, ref, at.centroids, at.bundle_id, at.thresh, "paper", "cfg0 paper")
     assert info["labelled"] > 500
 
 
@@ -71,7 +71,7 @@ def test_paper_cfg1_subset_parity():
     fib = fibers_for_config(1, 0, 4000)
     lab, d = _gpu(A, fib)
     ref = oracle.classify(fib, at.centroids, at.bundle_id, at.thresh, mode="paper")
-    check_parity(lab, d, ref, "cfg1[:4000] paper")
+    check_parity_full(lab, d, fib, ref, at.centroids, at.bundle_id, at.thresh, "paper", "cfg1[:4000] paper")
 
 
 @pytest.mark.parametrize("cfg,k", [(3, 2000), (4, 2000)])
@@ -83,7 +83,8 @@ def test_paper_full_size_sampled(cfg, k):
     lab, d = _gpu(A, fib)
     idx = sample_indices(fib.shape[0], k, seed=91)
     ref = oracle.classify(fib[idx], at.centroids, at.bundle_id, at.thresh, mode="paper")
-    check_parity(lab[idx], d[idx], ref, f"cfg{cfg} paper sample")
+    check_parity_full(lab[idx], d[idx], fib[idx], ref, at.centroids, at.bundle_id, at.thresh, "paper",
+                      f"cfg{cfg} paper sample")
 
 
 def test_paper_subset_of_exact_and_reversal(cfg0p):
@@ -124,3 +125,44 @@ def test_paper_host_buffers_equal_device(cfg0p):
     lab, d = _gpu(A, fib)
     hl, hd = A.classify(np.ascontiguousarray(fib))
     assert np.array_equal(hl, lab) and np.array_equal(hd.view(np.int32), d.view(np.int32))
+
+
+def _loop_fiber():
+    """A closed, non-palindromic loop with dyadic coordinates: a_0 = a_20, so every centroid's end-point
+    maxima tie exactly (tests/test_oracle_paper_pins.py)."""
+    t = np.arange(21, dtype=np.float64) * (2 * np.pi / 20)
+    f = np.stack([8 * np.cos(t) - 8, 6 * np.sin(t), 2 * np.sin(2 * t)], 1)
+    f = (np.round(f * 64) / 64).astype(np.float32)
+    f[20] = f[0]
+    return f
+
+
+def test_paper_tie_picks_the_callers_direct_orientation():
+    """seg_create stores some centroids reversed (canonical orientation within a bundle: the
+    orientation closer to the bundle's first member).  A loop fiber (a_0 = a_20) ties the end-point maxima
+    exactly against every centroid; the tie must pick the caller's direct orientation whatever the stored
+    one, as the oracle's 'ties -> direct' does, so the result cannot depend on the centroid order.  Order
+    [r, c] stores c reversed, order [c, r] stores it forward: both must give the same bits.  The oracle
+    marks the fiber undecidable (both orientations are correct answers, reading R20); the GPU's answer is
+    also required to be the tie-direct one."""
+    a = _loop_fiber()
+    c = a + np.float32([0, 0, 1])
+    c[20] += np.float32([0.25, 0, 0])                      # an open centroid: c_0 != c_20
+    r = c[::-1].copy() + np.float32([0, 0, 40])            # far away, opposite orientation
+    cents = np.stack([r, c]).astype(np.float32)
+    bid = np.array([0, 0], np.int32)
+    thr = np.array([4.0], np.float32)
+    assert oracle.orientation_ambiguous(a, c) and oracle.endpoint_orientation(a, c) == 0
+    direct = oracle.max_pointwise(a, c) + oracle.tn(oracle.polyline_length(a), oracle.polyline_length(c))
+    assert oracle.max_pointwise(a, c, inverse=True) > 5.0
+    bits = []
+    for order in ([0, 1], [1, 0]):
+        A = Atlas(torch.from_numpy(cents[order]).cuda(), torch.from_numpy(bid).cuda(), torch.from_numpy(thr).cuda(),
+                  mode="paper")
+        lab, d = _gpu(A, a[None])
+        ref = oracle.classify(a[None], cents[order], bid, thr, mode="paper")
+        assert ref["label"][0] == 0 and ref["dist"][0] == pytest.approx(direct, rel=1e-12) and not ref["decidable"][0]
+        assert lab[0] == 0 and abs(d[0] - direct) <= 1e-5 * direct, (order, lab, d, direct)
+        check_parity_full(lab, d, a[None], ref, cents[order], bid, thr, "paper", f"loop order {order}")
+        bits.append((int(lab[0]), int(d.view(np.int32)[0])))
+    assert bits[0] == bits[1]

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import oracle
-from parity_util import check_parity
+from parity_util import check_parity, check_parity_full
 from synth import CONFIGS, atlas_for_config, fibers_for_config, sample_indices
 
 pytestmark = pytest.mark.gpu
@@ -76,7 +76,7 @@ def test_cfg1_subset_full_parity():
     fib = fibers_for_config(1, 0, 6000)
     lab, d = _gpu(A, fib)
     ref = oracle.classify(fib, at.centroids, at.bundle_id, at.thresh)
-    check_parity(lab, d, ref, "cfg1[:6000]")
+    check_parity_full(lab, d, fib, ref, at.centroids, at.bundle_id, at.thresh, "exact", "cfg1[:6000]")
 
 
 @pytest.mark.parametrize("cfg,k", [(1, 5000), (2, 3000), (3, 3000), (4, 3000)])
@@ -89,7 +89,8 @@ def test_full_size_sampled_parity(cfg, k):
     lab, d = _gpu(A, fib)
     idx = sample_indices(fib.shape[0], k, seed=cfg)
     ref = oracle.classify(fib[idx], at.centroids, at.bundle_id, at.thresh)
-    info = check_parity(lab[idx], d[idx], ref, f"cfg{cfg} sampled")
+    info = check_parity_full(lab[idx], d[idx], fib[idx], ref, at.centroids, at.bundle_id, at.thresh, "exact",
+                             f"cfg{cfg} sampled")
     # properties that hold at any size: labelled -> dist <= thr; unlabelled -> +inf
     m = lab >= 0
     assert np.all(d[m] <= at.thresh[lab[m]])
