@@ -41,14 +41,14 @@ def _worker(rank, world, port, q):
     at = atlas_for_config(0) if rank == 0 else None
     c, b, t = broadcast_atlas(at, 500, 10, torch.device("cpu"), world)
     n = 301
-    fib = fibers_for_config(0, 0, n)
     lo, hi = shard_range(n, world, rank)
+    fib_shard = fibers_for_config(0, lo, hi)        # each rank generates only its shard, as bench.py does
 
     def classify(f):
         r = oracle.classify(f.numpy(), c.numpy(), b.numpy(), t.numpy(), threads=1)
         return torch.from_numpy(r["label"]), torch.from_numpy(r["dist"].astype(np.float32))
 
-    lab, d = classify_sharded(classify, torch.from_numpy(fib[lo:hi]), n, world, rank)
+    lab, d = classify_sharded(classify, torch.from_numpy(fib_shard), n, world, rank)
     q.put((rank, lab.numpy(), d.numpy(), c.numpy().sum()))
     dist.destroy_process_group()
 
