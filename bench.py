@@ -232,10 +232,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SEG_BENCH_ONE_DEVICE=1 + SEG_BENCH_BACKEND=gloo: a functional check of the multi-rank code path with every
+    # rank on cuda:0 (no rank waits on another's kernel; the collectives run on the host).  Not a timing
+    # configuration: the driver's runs use one GPU per rank and NCCL.
+    local_dev = 0 if os.environ.get("SEG_BENCH_ONE_DEVICE") == "1" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SEG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_1912_11494_b200 import Atlas, binding
     from paper_1912_11494_b200.dist import broadcast_atlas, classify_sharded, shard_range
@@ -290,7 +298,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         ev0.record(stream)
         for i in range(args.steps):
             if flush:
@@ -406,8 +414,9 @@ def main():
                    fibers_per_s=n_job / (e2e_ms * 1e-3),
                    h2d_bytes_per_step=int(fib_np.nbytes) * world, d2h_bytes_per_step=int(d2h),
                    steps=args.e2e_steps,
-                   path="library host-buffer pipeline (seg_classify, host pointers)" if world == 1 else
-                        "per rank: pinned H2D of its shard, seg_classify, NCCL all_gather; rank 0 D2H of all results")
+                   path=("library host-buffer pipeline (seg_classify, host pointers)" if world == 1 else
+                         "per rank: pinned H2D of its shard, seg_classify, NCCL all_gather; rank 0 D2H of all results"
+                         if strong else "per rank: pinned H2D of its subject, seg_classify, D2H of its results"))
 
     # ---------------- CPU baseline (oracle) on rank 0 at N=1 ----------------
     cpu = None

@@ -1,13 +1,24 @@
-"""Copy a gpu_round.sh run (gpurun_out/) into profiles/r01/: bench lines, launch list + shares, ncu summaries,
-and profiles/traffic.json (k_classify DRAM bytes from the full capture)."""
-import csv, collections, io, json, os, re, shutil, subprocess, sys
+"""Copy a scripts/gpu/ncu.sh run (gpurun_out/) into profiles/<round>/: the launch list and per-kernel shares,
+ncu summaries of k_classify (exact and paper mode) and k_cull, and profiles/traffic.json (k_classify DRAM
+bytes per launch from the full captures, keyed by config and mode).
+
+    python scripts/refresh_profiles.py r02
+"""
+import collections
+import csv
+import io
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles", "r01")
-for src, dst in (("bench.json", "bench_cfg3.json"), ("bench_ref.json", "bench_reference_cfg3.json"),
-                 ("bench_paper.json", "bench_cfg3_paper_mode.json"), ("bench_rows.jsonl", "bench_rows_cfg3.jsonl"),
-                 ("launches.csv", "launches_cfg3.csv")):
-    shutil.copy(os.path.join(G, src), os.path.join(P, dst))
+RND = sys.argv[1] if len(sys.argv) > 1 else "r02"
+G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles", RND)
+os.makedirs(P, exist_ok=True)
+shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, "launches_cfg3.csv"))
 
 rows = list(csv.reader(open(os.path.join(G, "launches.csv"))))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -31,24 +42,27 @@ out.append("(ncu --metrics gpu__time_duration.sum --clock-control none; cold-cac
 open(os.path.join(P, "launch_shares_cfg3.txt"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
 
-for rep, dst in (("prof_classify", "ncu_k_classify_summary.txt"), ("prof_cull", "ncu_k_cull_summary.txt")):
-    s = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), os.path.join(G, rep + ".ncu-rep"), "30"],
+tf = os.path.join(ROOT, "profiles", "traffic.json")
+t = json.load(open(tf)) if os.path.exists(tf) else {}
+for rep, dst, key in (("prof_classify", "ncu_k_classify_summary.txt", "cfg3_exact"),
+                      ("prof_classify_paper", "ncu_k_classify_paper_summary.txt", "cfg3_paper"),
+                      ("prof_cull", "ncu_k_cull_summary.txt", None)):
+    path = os.path.join(G, rep + ".ncu-rep")
+    if not os.path.exists(path):
+        continue
+    s = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), path, "30"],
                        capture_output=True, text=True).stdout
     open(os.path.join(P, dst), "w").write(s)
-
-raw = subprocess.run(["ncu", "-i", os.path.join(G, "prof_classify.ncu-rep"), "--page", "raw", "--csv", "--metrics",
-                      "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
-hdr, units, vals = rr[0], rr[1], rr[2]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-b = {}
-for n, u, v in zip(hdr, units, vals):
-    if n.startswith("dram__bytes"):
-        b[n] = float(v.replace(",", "")) * scale[u]
-tf = os.path.join(ROOT, "profiles", "traffic.json")
-t = json.load(open(tf))
-t["cfg3"]["bytes"] = int(round(sum(b.values())))
-t["cfg3"]["source"] = (f"profiles/r01/ncu_k_classify_summary.txt (dram__bytes_read.sum {b['dram__bytes_read.sum'] / 1e9:.6f} GB + "
-                       f"dram__bytes_write.sum {b['dram__bytes_write.sum'] / 1e6:.6f} MB, one ncu --set full capture at HEAD)")
+    if key is None:
+        continue
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    b = {n: float(v.replace(",", "")) * scale[u] for n, u, v in zip(rr[0], rr[1], rr[2]) if n.startswith("dram__bytes")}
+    t[key] = dict(bytes=int(round(sum(b.values()))), kernel="k_classify",
+                  source=(f"profiles/{RND}/{dst} (dram__bytes_read.sum {b['dram__bytes_read.sum'] / 1e9:.6f} GB + "
+                          f"dram__bytes_write.sum {b['dram__bytes_write.sum'] / 1e6:.6f} MB, one ncu --set full capture)"),
+                  algorithmic_bytes=4_145_000 * (252 + 8))
 json.dump(t, open(tf, "w"), indent=1)
-print(t)
+print(json.dumps(t, indent=1))
