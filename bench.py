@@ -61,6 +61,9 @@ def parse():
                     help="exact: Eq. 2 d_ME (north_star, default); paper: d_ME (inferred orientation) + TN, row f1")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: one subject sharded over the ranks (north_star); weak: one subject per rank")
+    ap.add_argument("--gather", choices=["nccl", "p2p"], default="nccl",
+                    help="strong scaling, N>1: NCCL all_gather of the results, or the fused gather (each rank's "
+                         "kernel epilogue stores into rank 0's buffer over NVLink, dist.PeerResults)")
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -246,7 +249,8 @@ def main():
             dist.init_process_group(backend)
 
     from paper_1912_11494_b200 import Atlas, binding
-    from paper_1912_11494_b200.dist import broadcast_atlas, classify_sharded, shard_range
+    from paper_1912_11494_b200.dist import (PeerResults, broadcast_atlas, classify_sharded, classify_sharded_p2p,
+                                            shard_range)
     from synth import CONFIGS, atlas_for_config, fibers_for_config
 
     cfg = args.config
@@ -277,7 +281,11 @@ def main():
     def classify_into(f, lb=None, ds=None):
         return atlas.classify(f, lb if lb is not None else lab, ds if ds is not None else dst)
 
+    peer = PeerResults(n_total, world, rank, dev) if (strong and world > 1 and args.gather == "p2p") else None
+
     def step():
+        if peer is not None:                                   # fused gather: epilogue stores into rank 0
+            return classify_sharded_p2p(atlas.classify, fib, peer)
         if strong and world > 1:
             return classify_sharded(lambda f: classify_into(f), fib, n_total, world, rank)   # + all_gather (C2)
         return classify_into(fib)
@@ -380,7 +388,9 @@ def main():
 
             def e2e_step():
                 fdev.copy_(hf, non_blocking=True)                # this rank's own H2D over its own link
-                if strong:
+                if peer is not None:
+                    lb, ds = classify_sharded_p2p(atlas.classify, fdev, peer)
+                elif strong:
                     lb, ds = classify_sharded(lambda f: classify_into(f), fdev, n_total, world, rank)
                 else:
                     lb, ds = classify_into(fdev)
@@ -415,7 +425,9 @@ def main():
                    h2d_bytes_per_step=int(fib_np.nbytes) * world, d2h_bytes_per_step=int(d2h),
                    steps=args.e2e_steps,
                    path=("library host-buffer pipeline (seg_classify, host pointers)" if world == 1 else
-                         "per rank: pinned H2D of its shard, seg_classify, NCCL all_gather; rank 0 D2H of all results"
+                         ("per rank: pinned H2D of its shard, seg_classify storing into rank 0 (fused gather); rank 0 "
+                          "D2H of all results" if peer is not None else
+                          "per rank: pinned H2D of its shard, seg_classify, NCCL all_gather; rank 0 D2H of all results")
                          if strong else "per rank: pinned H2D of its subject, seg_classify, D2H of its results"))
 
     # ---------------- CPU baseline (oracle) on rank 0 at N=1 ----------------
@@ -433,7 +445,9 @@ def main():
             config=dict(workload=workload_name(cfg, args.mode), fibers=n_job, fibers_per_gpu=N,
                         centroids=spec["n_centroids"], bundles=spec["n_bundles"],
                         parallelism=(f"one subject sharded contiguously over {world} ranks (atlas NCCL-broadcast, "
-                                     f"results all_gathered in every step)" if strong else
+                                     + ("results stored into rank 0 by each rank's kernel epilogue over NVLink "
+                                        "(fused gather)" if peer is not None else "results all_gathered (NCCL)")
+                                     + " in every step)" if strong else
                                      f"one full subject per rank x{world}"),
                         l2=(f"inputs {n_job * 252 / 1e9:.2f} GB > 2 x 126 MB L2; no flush needed" if not flush else
                             f"inputs {n_job * 252 / 1e6:.1f} MB: each step timed alone after a 256 MB L2 flush"),

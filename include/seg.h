@@ -98,7 +98,12 @@ int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M,
  * seg_classify -- label N fibers (Alg. 1 over all fibers).
  *   fibers float32 [N][21][3]; label int32 [N]; dist float32 [N].
  *   Either all three pointers are device memory on the atlas's device (the call is
- *   then ASYNCHRONOUS on `stream`, a cudaStream_t; NULL = legacy default stream), or
+ *   then ASYNCHRONOUS on `stream`, a cudaStream_t; NULL = legacy default stream) -- label and dist
+ *   may also be device memory of a PEER GPU the atlas's device can access (e.g. rank 0's result
+ *   buffer mapped through CUDA IPC): the kernel's epilogue then stores each fiber's result straight
+ *   into that GPU's memory over NVLink, which fuses the multi-GPU gather (SURVEY.md Sec. 8(e),
+ *   PAPER.md:152 "no collision problems": one slot per fiber); the caller orders the completion
+ *   (e.g. a stream-ordered collective after the call) before the peer reads -- or
  *   all three are host memory (pinned or pageable): the call then streams chunks
  *   host->device, classifies and copies the results back, overlapping the copies
  *   with the kernel, and returns after the results are in host memory.
@@ -112,7 +117,8 @@ int seg_create_ex(const float *centroids, const int32_t *bundle_id, int64_t M,
  *   Morton key, bucket rank, permutation, seed code -- plus 2 (T + 2) B per 256 fibers); fibers are independent, so the slicing changes no result.
  *   N = 0 is a no-op returning SEG_OK.
  * Errors: SEG_EINVAL (null atlas, null pointer with N > 0, N > 2^31 - 1, mixed host
- * and device pointers, a device pointer on another device, misalignment),
+ * and device pointers, fibers on another device, label / dist on a device the atlas's device
+ * cannot access, misalignment),
  * SEG_ENOMEM, SEG_ECUDA (launch failure).  Asynchronous execution faults surface
  * at the caller's next synchronisation.
  */

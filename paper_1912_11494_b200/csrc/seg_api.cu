@@ -762,8 +762,24 @@ int classify_common(const seg_atlas *a, const float *fibers, int64_t N, int32_t 
     const int k0 = pointer_kind(fibers, &d0), k1 = pointer_kind(label, &d1), k2 = pointer_kind(dist, &d2);
     if (k0 < 0 || k1 < 0 || k2 < 0) return fail(SEG_ECUDA, "seg_classify: no usable CUDA device");
     if (k0 != k1 || k0 != k2) return fail(SEG_EINVAL, "seg_classify: fibers/label/dist mix host and device memory");
-    if (k0 == 1 && (d0 != a->device || d1 != a->device || d2 != a->device))
+    if (k0 == 1 && d0 != a->device)
         return fail(SEG_EINVAL, "seg_classify: device pointer not on the atlas's device");
+    if (k0 == 1) {
+        // label / dist may live on a peer GPU the atlas's device can access (the fused gather, seg.h)
+        for (int d : {d1, d2}) {
+            if (d == a->device) continue;
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, a->device, d) != cudaSuccess || !ok) {
+                cudaGetLastError();
+                return fail(SEG_EINVAL, "seg_classify: label / dist on a device the atlas's device cannot access");
+            }
+            DeviceGuard pg(a->device);   // the kernel runs on the atlas's device: map the peer into it (idempotent)
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(d, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+                return cuda_fail(pe, "seg_classify: cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    }
     DeviceGuard guard(a->device);
     if (!guard.ok) return fail(SEG_ECUDA, "seg_classify: cudaSetDevice failed");
     cudaStream_t s = (cudaStream_t)stream;

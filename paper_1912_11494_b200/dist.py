@@ -5,7 +5,9 @@ PAPER.md:152), so the data path needs no collective: each rank classifies its ow
 contiguous shard.  The only exchanges are
   * the atlas, replicated once at setup by a broadcast from rank 0 (C1), and
   * optionally the labels, gathered after the classification (C2).
-Shard boundaries are multiples of 4 fibers so every shard starts 16-byte aligned.
+Shard boundaries are multiples of 4 fibers so every shard starts 16-byte aligned.  The gather is
+either NCCL's all_gather (classify_sharded) or fused into the classify kernel's epilogue, which stores
+each fiber's result straight into rank 0's memory over NVLink (PeerResults, classify_sharded_p2p).
 
 Row f4: the atlas can be sharded instead (atlases beyond one GPU, or more GPUs
 than subjects): every rank holds a subset of the bundles (shard_bundles / shard_atlas) and writes
@@ -67,6 +69,44 @@ def classify_sharded(classify, fibers: torch.Tensor, n_total: int, world: int, r
         rows.append(out[r * chunk: r * chunk + (b - a)])
     full = torch.cat(rows)
     return full[:, 0].contiguous(), full[:, 1].contiguous().view(torch.float32)
+
+
+class PeerResults:
+    """The fused gather (the NVLink-native option for C2): rank 0 owns the whole
+    subject's label int32[n] / dist float32[n]; every other rank maps them through CUDA IPC, so each rank's
+    seg_classify epilogue stores its shard's results straight into rank 0's memory over NVLink (include/seg.h:
+    label / dist may be peer memory).  One slot per fiber, so no two ranks ever write the same word
+    (PAPER.md:152).  The IPC handles travel once, at setup, as pickled torch IPC descriptors."""
+
+    def __init__(self, n_total: int, world: int, rank: int, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.n, self.world, self.rank = n_total, world, rank
+        if rank == 0:
+            self.label = torch.empty(n_total, dtype=torch.int32, device=device)
+            self.dist = torch.empty(n_total, dtype=torch.float32, device=device)
+            desc = [reduce_tensor(self.label), reduce_tensor(self.dist)]
+        else:
+            desc = [None, None]
+        if world > 1:
+            dist.broadcast_object_list(desc, src=0)
+        if rank != 0:
+            with torch.cuda.device(device):
+                self.label = desc[0][0](*desc[0][1])
+                self.dist = desc[1][0](*desc[1][1])
+        lo, hi = shard_range(n_total, world, rank)
+        self.my_label, self.my_dist = self.label[lo:hi], self.dist[lo:hi]
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def classify_sharded_p2p(classify_into, fibers: torch.Tensor, peer: PeerResults):
+    """This rank's shard classified with its results stored straight into rank 0's buffers (fused gather),
+    then a stream-ordered one-element all_reduce that completes only after every rank's kernel did, so rank
+    0's later work on the same stream sees every shard.  classify_into(fibers, label, dist) is
+    Atlas.classify.  Returns rank 0's full (label, dist) on rank 0, this rank's views elsewhere."""
+    classify_into(fibers, peer.my_label, peer.my_dist)
+    if peer.world > 1:
+        dist.all_reduce(peer.flag)
+    return (peer.label, peer.dist) if peer.rank == 0 else (peer.my_label, peer.my_dist)
 
 
 def shard_bundles(counts, world: int) -> list:
