@@ -334,7 +334,18 @@ constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 #define SEG_FB_PAPER 2
 #endif
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
-constexpr int Q2CAP = 192;             // candidate stack; flushed when fewer than 64 slots remain
+// pitch of one point's plane (32 fibers) in the per-warp fxy (float2) and fz (float) arrays.  33, not 32: the
+// ingest's 4-byte cp.async of one fiber by 32 lanes writes one coordinate of ~10 different points, which at
+// pitch 32 all fall into the same bank (10x the ideal wavefronts, ncu r02); at 33 they spread over the banks.
+// Reads of one point by 32 lanes (different fibers) stay conflict-free either way.
+#ifndef SEG_PLANE_PITCH
+#define SEG_PLANE_PITCH 33
+#endif
+constexpr int PP = SEG_PLANE_PITCH;
+#ifndef SEG_Q2CAP
+#define SEG_Q2CAP 184
+#endif
+constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (184: room for the plane pitch)
 constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
@@ -361,8 +372,8 @@ struct SmemLayout {
     __host__ __device__ constexpr SmemLayout() {
         size_t o = 0;
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
-        fxy = o;  o += (size_t)NCW * NMID * 32 * sizeof(float2);
-        fz = o;   o += (size_t)NCW * NMID * 32 * sizeof(float);
+        fxy = o;  o += (size_t)NCW * NMID * PP * sizeof(float2);
+        fz = o;   o += (size_t)NCW * NMID * PP * sizeof(float);
         fe = o;   o += (size_t)FPC * sizeof(float4);   // (x0, x20, y0, y20)
         fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = h10 (NaN: a non-finite fiber)
         fez = o;  o += (size_t)FPC * sizeof(float4);   // (z0, z20, h0, h20): h = lowered half norms
@@ -450,8 +461,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     const int cta = p.cta_order ? __ldg(p.cta_order + blockIdx.x) : (int)blockIdx.x;
     SEG_DCHECK(cta >= 0 && (size_t)cta * FPC < (size_t)p.n);
     const int cw = consumer ? warp : 0;
-    float2 *fxy = reinterpret_cast<float2 *>(smem + L.fxy) + cw * (NMID * 32);   // [18][32]
-    float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NMID * 32);       // [18][32]
+    float2 *fxy = reinterpret_cast<float2 *>(smem + L.fxy) + cw * (NMID * PP);   // [18][PP]
+    float *fz = reinterpret_cast<float *>(smem + L.fz) + cw * (NMID * PP);       // [18][PP]
     float4 *fe = fe_all + cw * 32;
     float4 *fm = fm_all + cw * 32;
     float4 *fez = fez_all + cw * 32;
@@ -501,9 +512,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 return reinterpret_cast<float *>(fez) + (pt == 20 ? 1 : 0);
             }
             if (pt == 10) { stride = 4; return reinterpret_cast<float *>(fm) + c; }
-            if (c < 2) { stride = 2; return reinterpret_cast<float *>(fxy + mid_slot(pt) * 32) + c; }
+            if (c < 2) { stride = 2; return reinterpret_cast<float *>(fxy + mid_slot(pt) * PP) + c; }
             stride = 1;
-            return fz + mid_slot(pt) * 32;
+            return fz + mid_slot(pt) * PP;
         };
         int s0 = 1, s1 = 1;
         float *d0 = plane(k0, s0), *d1 = plane(k1 < 3 * NPTS ? k1 : 0, s1);
@@ -540,8 +551,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 if (i == 0) return make_float4(fe[lane].x, fe[lane].z, fez[lane].x, 0.f);
                 if (i == 20) return make_float4(fe[lane].y, fe[lane].w, fez[lane].y, 0.f);
                 if (i == 10) return fm[lane];
-                const float2 a = fxy[mid_slot(i) * 32 + lane];
-                return make_float4(a.x, a.y, fz[mid_slot(i) * 32 + lane], 0.f);
+                const float2 a = fxy[mid_slot(i) * PP + lane];
+                return make_float4(a.x, a.y, fz[mid_slot(i) * PP + lane], 0.f);
             };
             float len = 0.f;
             float4 prev = pt(0);
@@ -586,8 +597,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
 #pragma unroll
             for (int i = 1; i < NPTS - 1; ++i) {
                 if (i == 10) continue;
-                const float2 a = fxy[mid_slot(i) * 32 + lane];
-                r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + lane], __ldg(cc + (o ? NPTS - 1 - i : i))));
+                const float2 a = fxy[mid_slot(i) * PP + lane];
+                r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + lane], __ldg(cc + (o ? NPTS - 1 - i : i))));
             }
             if (PAPER) {
                 // score = d_ME + TN (Eq. 3), the lengths as the candidate rounds take them
@@ -672,8 +683,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                     bool done = false;
 #define SEG_STEP(i)                                                             \
     {                                                                           \
-const float2 a = fxy[mid_slot(i) * 32 + fl];                            \
-r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * 32 + fl], cb[(i) * st]));    \
+const float2 a = fxy[mid_slot(i) * PP + fl];                            \
+r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
     }
                     if (STATS) cnt[ST_T34]++;
                     SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
