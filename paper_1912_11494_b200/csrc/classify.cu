@@ -342,6 +342,9 @@ constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (sme
 #define SEG_PLANE_PITCH 33
 #endif
 constexpr int PP = SEG_PLANE_PITCH;
+#ifndef SEG_PLANE_SKEW
+#define SEG_PLANE_SKEW 16
+#endif
 #ifndef SEG_Q2CAP
 #define SEG_Q2CAP 184
 #endif
@@ -374,8 +377,10 @@ struct SmemLayout {
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
         fxy = o;  o += (size_t)NCW * NMID * PP * sizeof(float2);
         fz = o;   o += (size_t)NCW * NMID * PP * sizeof(float);
-        fe = o;   o += (size_t)FPC * sizeof(float4);   // (x0, x20, y0, y20)
-        fm = o;   o += (size_t)FPC * sizeof(float4);   // point 10, w = h10 (NaN: a non-finite fiber)
+        // fe / fm / fez 16 B apart in bank alignment, so the ingest's writes of x0, x10, z0 (etc.) of one
+        // fiber do not share a bank (bank model: 3.3 -> 2.3 wavefronts per ingest instruction)
+        fe = o;   o += (size_t)FPC * sizeof(float4) + SEG_PLANE_SKEW;   // (x0, x20, y0, y20)
+        fm = o;   o += (size_t)FPC * sizeof(float4) + SEG_PLANE_SKEW;   // point 10, w = h10 (NaN: a non-finite fiber)
         fez = o;  o += (size_t)FPC * sizeof(float4);   // (z0, z20, h0, h20): h = lowered half norms
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
         flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
@@ -810,7 +815,13 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         const float4 E = fe[j];
                         const float4 Ez = fez[j];
                         const float4 a10 = fm[j];
+#ifdef SEG_VOTE_JJ
                         const float tj = __shfl_sync(0xffffffffu, tcmp, j);
+#else
+                        // an empty slot (j = -1) gets a NaN cutoff: every comparison with it is false, so its
+                        // garbage values drop out without a jj >= 0 test on the vote's dependent chain
+                        const float tj = j >= 0 ? __shfl_sync(0xffffffffu, tcmp, j) : __int_as_float(0x7fffffff);
+#endif
                         const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)),
                                   EZ = f2u(make_float2(Ez.x, Ez.y));
                         float m10;
@@ -842,7 +853,11 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         tjv[q] = tj;
                         // one VOTE.ANY per fiber: far shorter latency than a REDUX.OR of the step's bits
                         // (cfg 3: -3.6%)
+#ifdef SEG_VOTE_JJ
                         if (__any_sync(0xffffffffu, jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
+#else
+                        if (__any_sync(0xffffffffu, fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
+#endif
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
 #if defined(SEG_EXP) && SEG_EXP == 3
