@@ -22,6 +22,8 @@
 #include <climits>
 #include <cstdint>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "seg_internal.cuh"
 
 namespace seg {
@@ -248,6 +250,50 @@ __global__ void k_morton_scatter(MortonParams p) {
     const uint32_t pos = __ldg(p.hist + k) + p.rank[i] + __ldg(p.bsum + k / SCAN_B);
     SEG_DCHECK(pos < (uint32_t)p.n);
     p.perm[pos] = i;
+}
+
+// The prepass as a radix sort instead: k_morton_key writes every fiber's key and its index, and CUB's
+// onesweep radix sort (stable, 3 x bits key bits) orders the indices.  The histogram form above serialises its
+// atomics on the crowded cells (matched fibers cluster around the bundles' midpoints: k_morton_hist 179 us
+// at cfg 3); the sort has no hot spots.  Stable, so the order inside a cell is the input order.
+__global__ void k_morton_key(MortonParams p) {
+    const float lim = (float)((1 << p.bits) - 1);
+    const float sc = (float)(1 << (p.bits - MORTON_BITS));
+    const int i0 = blockIdx.x * blockDim.x * MORTON_FPT + threadIdx.x;
+    float v[MORTON_FPT][3];
+#pragma unroll
+    for (int q = 0; q < MORTON_FPT; ++q) {
+        const int i = i0 + q * blockDim.x;
+        const float *f = p.fibers + (size_t)min(i, p.n - 1) * (3 * NPTS) + 30;  // point 10
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[q][c] = __ldg(f + c);
+    }
+#pragma unroll
+    for (int q = 0; q < MORTON_FPT; ++q) {
+        const int i = i0 + q * blockDim.x;
+        if (i >= p.n) break;
+        const float qx = fminf(fmaxf((v[q][0] - p.lo.x) * (p.inv_cell.x * sc), 0.f), lim);
+        const float qy = fminf(fmaxf((v[q][1] - p.lo.y) * (p.inv_cell.y * sc), 0.f), lim);
+        const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * (p.inv_cell.z * sc), 0.f), lim);
+        p.key[i] = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
+        p.rank[i] = (uint32_t)i;   // the value the sort carries
+    }
+}
+
+size_t morton_sort_temp_bytes(int n, int bits) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, n, 0, 3 * bits);
+    return bytes;
+}
+
+cudaError_t launch_morton_sort(const MortonParams &p, uint32_t *keys_out, void *temp, size_t temp_bytes,
+                               cudaStream_t s) {
+    k_morton_key<<<(p.n + 256 * MORTON_FPT - 1) / (256 * MORTON_FPT), 256, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, p.key, keys_out, reinterpret_cast<const int32_t *>(p.rank),
+                                           p.perm, p.n, 0, 3 * p.bits, s);
 }
 
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
@@ -815,13 +861,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         const float4 E = fe[j];
                         const float4 Ez = fez[j];
                         const float4 a10 = fm[j];
-#ifdef SEG_VOTE_JJ
                         const float tj = __shfl_sync(0xffffffffu, tcmp, j);
-#else
-                        // an empty slot (j = -1) gets a NaN cutoff: every comparison with it is false, so its
-                        // garbage values drop out without a jj >= 0 test on the vote's dependent chain
-                        const float tj = j >= 0 ? __shfl_sync(0xffffffffu, tcmp, j) : __int_as_float(0x7fffffff);
-#endif
                         const u64 EX = f2u(make_float2(E.x, E.y)), EY = f2u(make_float2(E.z, E.w)),
                                   EZ = f2u(make_float2(Ez.x, Ez.y));
                         float m10;
@@ -853,11 +893,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         tjv[q] = tj;
                         // one VOTE.ANY per fiber: far shorter latency than a REDUX.OR of the step's bits
                         // (cfg 3: -3.6%)
-#ifdef SEG_VOTE_JJ
                         if (__any_sync(0xffffffffu, jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
-#else
-                        if (__any_sync(0xffffffffu, fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
-#endif
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
 #if defined(SEG_EXP) && SEG_EXP == 3
