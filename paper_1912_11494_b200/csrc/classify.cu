@@ -487,10 +487,19 @@ __device__ __forceinline__ float box_d2(float x, float y, float z, const float4 
 __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez, const float4 &F10,
                                               const TileHdr &h, float s) {
     const float s2 = s * s;
+#ifdef SEG_BOX_SHORTCIRCUIT
     const bool p10 = box_d2(F10.x, F10.y, F10.z, h.lo10, h.hi10) <= s2;
     const bool pdir = box_d2(E.x, E.z, Ez.x, h.lo0, h.hi0) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo20, h.hi20) <= s2;
     const bool pinv = box_d2(E.x, E.z, Ez.x, h.lo20, h.hi20) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo0, h.hi0) <= s2;
     return p10 && (pdir || pinv);
+#else
+    // all five box distances, combined without short-circuits: the && form compiled to branches that
+    // diverge across the warp's fibers (ncu r02: a third of the kernel's divergent branches)
+    const bool p10 = box_d2(F10.x, F10.y, F10.z, h.lo10, h.hi10) <= s2;
+    const bool d0 = box_d2(E.x, E.z, Ez.x, h.lo0, h.hi0) <= s2, d20 = box_d2(E.y, E.w, Ez.y, h.lo20, h.hi20) <= s2;
+    const bool i0 = box_d2(E.x, E.z, Ez.x, h.lo20, h.hi20) <= s2, i20 = box_d2(E.y, E.w, Ez.y, h.lo0, h.hi0) <= s2;
+    return p10 & ((d0 & d20) | (i0 & i20));
+#endif
 }
 
 template <bool STATS, bool PAPER>
@@ -1076,10 +1085,19 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
                         const float d10 = d2(F10.x, F10.y, F10.z, ct.c10);
                         const float d00 = d2(E.x, E.z, Ez.x, ct.c0), d2020 = d2(E.y, E.w, Ez.y, ct.c20);
                         const float d020 = d2(E.x, E.z, Ez.x, ct.c20), d200 = d2(E.y, E.w, Ez.y, ct.c0);
+#ifdef SEG_CULL_SHORTCIRCUIT
                         const bool pass = bpass && d10 <= ct.c10.w &&
                                           ((d00 <= ct.c0.w && d2020 <= ct.c20.w) || (d020 <= ct.c20.w && d200 <= ct.c0.w));
                         const bool close = pass && d10 <= ct.q.y &&
                                            ((d00 <= ct.q.x && d2020 <= ct.q.z) || (d020 <= ct.q.z && d200 <= ct.q.x));
+#else
+                        // non-short-circuit & / |: the && form compiled to branches diverging across the warp's
+                        // fibers (ncu r02: 83% of k_cull's divergent branches on these two lines)
+                        const bool pass = bpass & (d10 <= ct.c10.w) &
+                                          (((d00 <= ct.c0.w) & (d2020 <= ct.c20.w)) | ((d020 <= ct.c20.w) & (d200 <= ct.c0.w)));
+                        const bool close = pass & (d10 <= ct.q.y) &
+                                           (((d00 <= ct.q.x) & (d2020 <= ct.q.z)) | ((d020 <= ct.q.z) & (d200 <= ct.q.x)));
+#endif
                         pm |= (pass ? 1u : 0u) << j;
                         cm |= (close ? 1u : 0u) << j;
                         const float dc = fmaxf(d10, fminf(fmaxf(d00, d2020), fmaxf(d020, d200)));
