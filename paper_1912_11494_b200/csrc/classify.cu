@@ -44,6 +44,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void cp_async4(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// the same with src-size operand n (0 or 4): n = 0 copies nothing and writes 4 zero bytes (no global read)
+__device__ __forceinline__ void cp_async4_n(void *dst, const void *src, uint32_t n) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -577,7 +581,16 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             return fz + mid_slot(pt) * PP;
         };
         int s0 = 1, s1 = 1;
+#ifdef SEG_INGEST_BRANCH
         float *d0 = plane(k0, s0), *d1 = plane(k1 < 3 * NPTS ? k1 : 0, s1);
+#else
+        // lane 31 has no second value (63 floats per fiber): it zero-fills a slot of flen instead (written
+        // after the ingest in paper mode, unused in exact mode), so the loops below need no branch on k1
+        float *d0 = plane(k0, s0), *d1 = k1 < 3 * NPTS ? plane(k1, s1) : flen;
+        if (k1 >= 3 * NPTS) s1 = 1;
+        const uint32_t n1 = k1 < 3 * NPTS ? 4u : 0u;
+        const int k1s = k1 < 3 * NPTS ? k1 : 3 * NPTS - 1;
+#endif
         int fjs = -1;
 #pragma unroll INGEST_UNROLL
         for (int j = 0; j < 32; ++j) {
@@ -586,14 +599,22 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             if (fj >= 0) {
                 const float *src = p.fibers + (size_t)fj * (3 * NPTS);
                 cp_async4(d0 + j * s0, src + k0);
+#ifdef SEG_INGEST_BRANCH
                 if (k1 < 3 * NPTS) cp_async4(d1 + j * s1, src + k1);
+#else
+                cp_async4_n(d1 + j * s1, src + k1s, n1);
+#endif
             }
         }
         cp_async_wait_all();
         uint32_t fin = 0;   // bit j: this lane's two values of fiber j are finite
 #pragma unroll INGEST_UNROLL
         for (int j = 0; j < 32; ++j) {
+#ifdef SEG_INGEST_BRANCH
             const bool ok = isfinite(d0[j * s0]) && (k1 >= 3 * NPTS || isfinite(d1[j * s1]));
+#else
+            const bool ok = isfinite(d0[j * s0]) & isfinite(d1[j * s1]);
+#endif
             fin |= (ok ? 1u : 0u) << j;
         }
         fin = __reduce_and_sync(0xffffffffu, fin);   // bit j: every value of fiber j is finite
@@ -1085,19 +1106,10 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
                         const float d10 = d2(F10.x, F10.y, F10.z, ct.c10);
                         const float d00 = d2(E.x, E.z, Ez.x, ct.c0), d2020 = d2(E.y, E.w, Ez.y, ct.c20);
                         const float d020 = d2(E.x, E.z, Ez.x, ct.c20), d200 = d2(E.y, E.w, Ez.y, ct.c0);
-#ifdef SEG_CULL_SHORTCIRCUIT
                         const bool pass = bpass && d10 <= ct.c10.w &&
                                           ((d00 <= ct.c0.w && d2020 <= ct.c20.w) || (d020 <= ct.c20.w && d200 <= ct.c0.w));
                         const bool close = pass && d10 <= ct.q.y &&
                                            ((d00 <= ct.q.x && d2020 <= ct.q.z) || (d020 <= ct.q.z && d200 <= ct.q.x));
-#else
-                        // non-short-circuit & / |: the && form compiled to branches diverging across the warp's
-                        // fibers (ncu r02: 83% of k_cull's divergent branches on these two lines)
-                        const bool pass = bpass & (d10 <= ct.c10.w) &
-                                          (((d00 <= ct.c0.w) & (d2020 <= ct.c20.w)) | ((d020 <= ct.c20.w) & (d200 <= ct.c0.w)));
-                        const bool close = pass & (d10 <= ct.q.y) &
-                                           (((d00 <= ct.q.x) & (d2020 <= ct.q.z)) | ((d020 <= ct.q.z) & (d200 <= ct.q.x)));
-#endif
                         pm |= (pass ? 1u : 0u) << j;
                         cm |= (close ? 1u : 0u) << j;
                         const float dc = fmaxf(d10, fminf(fmaxf(d00, d2020), fmaxf(d020, d200)));
