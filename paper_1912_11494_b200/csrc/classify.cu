@@ -375,10 +375,10 @@ constexpr int CULL_UNROLL = SEG_CULL_UNROLL;     // k_cull's 32-tile chunk loop
 constexpr int RANK_UNROLL = SEG_RANK_UNROLL;     // k_cull's best-first ranking loop
 constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
-// the dot-product screen: 2 (cfg 3: 3 -> +1.3%, 4 -> +1.1%, 1 -> +5.4%; the screen's shorter chains
-// make the smaller step pay).  Paper mode, d2 form, with the per-fiber VOTE: 2 as well (3: +2.1%).
+// the dot-product screen: 1 since round 2's bank-conflict and branch fixes (cfg 3 -1.1%, cfg 4 -1.6% vs 2;
+// 3: +1.5%); round 1 had measured 2 best.  Paper mode, d2 form, with the per-fiber VOTE: 2 (1: +0.9%).
 #ifndef SEG_FB
-#define SEG_FB 2
+#define SEG_FB 1
 #endif
 #ifndef SEG_FB_PAPER
 #define SEG_FB_PAPER 2
