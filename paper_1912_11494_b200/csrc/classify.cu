@@ -124,6 +124,18 @@ constexpr bool SCREEN_OFF = true;
 #else
 constexpr bool SCREEN_OFF = false;
 #endif
+// Paper mode screens too (round 2): the dense loop keeps every orientation whose screened 3-point estimate
+// passes (a superset, as in exact mode) and the candidate rounds take the end-point orientation decision on
+// the exact FP32 distances, dropping the other orientation.  -DSEG_PAPER_D2: the round-1 form (exact d2 in
+// the dense loop, the orientation decided there).
+#ifdef SEG_PAPER_D2
+constexpr bool PAPER_D2 = true;
+#else
+constexpr bool PAPER_D2 = false;
+#endif
+// the tile image's w slots (seg_create): 0 / 10 / 20 the screen's half norms; paper mode: 1 the centroid's
+// chord length, 2 the stored-reversed flag
+constexpr int W_LEN = 1, W_FLIP = 2;
 // Exact mode's dot-product screen (seg_internal.cuh): h = (s + ...) - a.c for the two fiber points packed
 // in (px, py, pz) against the scalar centroid point q, s = the packed sums of the lowered half norms.
 // Never above d2 / 2 (see there).
@@ -668,7 +680,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float4 c0p = __ldg(cc), c20p = __ldg(cc + NPTS - 1);
                 const float e00 = d2(E.x, E.z, Ez.x, c0p), e2020 = d2(E.y, E.w, Ez.y, c20p);
                 const float e020 = d2(E.x, E.z, Ez.x, c20p), e200 = d2(E.y, E.w, Ez.y, c0p);
-                const float flip = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + 20 * TILE + c).w;
+                const float flip = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + W_FLIP * TILE + c).w;
                 const float mi = fmaxf(e020, e200), md = fmaxf(e00, e2020);
                 o = (mi < md || (mi == md && flip != 0.f)) ? 1 : 0;
             }
@@ -683,7 +695,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             }
             if (PAPER) {
                 // score = d_ME + TN (Eq. 3), the lengths as the candidate rounds take them
-                const float clen = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + c).w;
+                const float clen = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + W_LEN * TILE + c).w;
                 const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[lane], clen));
                 // the same acceptance as a candidate of the tile stream: r <= thr2, then score <= thr
                 if (r <= __ldg(&h->thr2) && sc <= __ldg(&h->thr)) {
@@ -743,8 +755,22 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
                 float r;
-                if (PAPER) {
+                bool keep = true;
+                if (PAPER && PAPER_D2) {
                     r = qr[lane];
+                } else if (PAPER) {
+                    // the paper's orientation (R17): argmin of the exact end-point maxima, an
+                    // exact tie -> the caller's direct orientation; a candidate of the other orientation
+                    // (kept only by the screen's superset) drops out here
+                    const float4 a10 = fm[fl], E = fe[fl], Ez = fez[fl];
+                    const float4 *cq = T + c;
+                    const float4 q0 = cq[0], q20 = cq[20 * TILE];
+                    const float e00 = d2(E.x, E.z, Ez.x, q0), e2020 = d2(E.y, E.w, Ez.y, q20);
+                    const float e020 = d2(E.x, E.z, Ez.x, q20), e200 = d2(E.y, E.w, Ez.y, q0);
+                    const float mi = fmaxf(e020, e200), md = fmaxf(e00, e2020);
+                    const int oinf = (mi < md || (mi == md && cq[W_FLIP * TILE].w != 0.f)) ? 1 : 0;
+                    keep = o == oinf;
+                    r = fmaxf(d2(a10.x, a10.y, a10.z, cq[10 * TILE]), o ? mi : md);
                 } else {
                     // exact mode screened with estimates: the 3-point running max, exactly as the
                     // dense test2 of the d2 form computes it (d2 and d2_pair_b agree bit for bit)
@@ -758,7 +784,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
                 const float taul = fminf(thr2, key_cut2<PAPER>(best[fl]));
-                if (r <= taul) {  // re-check against the freshest best (best-first pays here)
+                if (keep && r <= taul) {  // re-check against the freshest best (best-first pays here)
                     const float4 *cb = T + c + (o ? 20 * TILE : 0);
                     const int st = o ? -TILE : TILE;
                     bool done = false;
@@ -788,7 +814,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         // a7: lexicographic (d^2, bundle) minimum; paper mode: (d_ME + TN, bundle)
                         if (PAPER) {
                             if (r <= taul) {
-                                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[c].w));
+                                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[W_LEN * TILE + c].w));
                                 if (sc <= thr) {
                                     const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b;
                                     if (excl) { if (kk < best[fl]) best[fl] = kk; } else
@@ -838,7 +864,8 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
             long long ts0 = 0;
             if (STATS) ts0 = clock64();
             const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
-            const float tcmp = (PAPER || SCREEN_OFF) ? tau : __fmul_rn(tau, 0.5f);   // exact mode screens at half scale
+            constexpr bool D2FORM = SCREEN_OFF || (PAPER && PAPER_D2);
+            const float tcmp = D2FORM ? tau : __fmul_rn(tau, 0.5f);   // the screen works at half scale
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
             // MUFU.SQRT (relative error < 2^-22) raised by 2^-20 so the radius never falls below the
             // exact one: no IEEE slow-path branch on the per-tile chain
@@ -896,7 +923,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                                   EZ = f2u(make_float2(Ez.x, Ez.y));
                         float m10;
                         float2 R0, R20;
-                        if (PAPER || SCREEN_OFF) {
+                        if (D2FORM) {
                             m10 = d2(a10.x, a10.y, a10.z, c10);                         // test1
                             R0 = d2_pair_b(EX, EY, EZ, c0.x, c0.y, c0.z);               // (e0,0, e20,0)
                             R20 = d2_pair_b(EX, EY, EZ, c20.x, c20.y, c20.z);           // (e0,20, e20,20)
@@ -911,13 +938,13 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         }
                         rdv[q] = fmaxf(fmaxf(m10, R0.x), R20.y);                        // test2, direct
                         riv[q] = fmaxf(fmaxf(m10, R20.x), R0.y);                        // test2, inverse
-                        if (PAPER) {
+                        if (PAPER && PAPER_D2) {
                             // the paper infers the direction from the end points:
                             // argmin of the end-point maxima, ties -> the caller's direct orientation
-                            // (reading R17; c20.w = 1 marks a centroid stored reversed); only that
+                            // (reading R17; the W_FLIP slot marks a centroid stored reversed); only that
                             // orientation goes on
                             const float mi = fmaxf(R20.x, R0.y), md = fmaxf(R0.x, R20.y);
-                            if (mi < md || (mi == md && c20.w != 0.f)) rdv[q] = INFINITY;
+                            if (mi < md || (mi == md && T[W_FLIP * TILE + lane].w != 0.f)) rdv[q] = INFINITY;
                             else riv[q] = INFINITY;
                         }
                         tjv[q] = tj;
@@ -948,7 +975,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         // the winner's orientation, chosen before the clamp below (a clamped negative
                         // screen value would no longer compare equal to rd)
                         const int wo = (ad && (!ai || rd <= ri)) ? 0 : 1;
-                        if (!PAPER) sc = fmaxf(sc, 0.f);   // screen values may be < 0; keep the key order
+                        if (!D2FORM) sc = fmaxf(sc, 0.f);   // screen values may be < 0; keep the key order
                         // the lane rides in the score's 5 low mantissa bits: REDUX.MIN names the winner
                         // directly (a heuristic choice; every survivor is still evaluated)
                         const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
@@ -959,7 +986,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         SEG_DCHECK(np < PECAP && j >= 0 && j < 32);
                         if (win) {
                             pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
-                            if (PAPER) pr[np] = sc;   // exact mode: the round re-evaluates the 3 points
+                            if (PAPER && PAPER_D2) pr[np] = sc;   // otherwise the round re-evaluates the 3 points
                         }
                         ++np;
                         const bool qd = ad && !(win && wo == 0), qi = ai && !(win && wo == 1);
@@ -967,12 +994,12 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         if (qd) {
                             const int pos = n2 + __popc(bd & lt_mask);
                             q2e[pos] = (uint16_t)e;
-                            if (PAPER) q2r[pos] = rd;
+                            if (PAPER && PAPER_D2) q2r[pos] = rd;
                         }
                         if (qi) {
                             const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
                             q2e[pos] = (uint16_t)(e | (1u << 10));
-                            if (PAPER) q2r[pos] = ri;
+                            if (PAPER && PAPER_D2) q2r[pos] = ri;
                         }
                         n2 += __popc(bd) + __popc(bi);
                         SEG_DCHECK(n2 <= Q2CAP);

@@ -415,13 +415,13 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
             for (int i = 0; i < NPTS; ++i) {
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
-                // w: paper mode -- point 0 carries the chord length (Eq. 3), point 20 a 1 when the centroid is
-                // stored reversed (an exact end-point tie then picks the caller's direct orientation, so the
-                // result does not depend on the stored order); exact mode -- points 0, 10, 20 carry the
-                // lowered half squared norm of k_classify's dot-product screen (seg_internal.cuh)
+                // w: points 0, 10, 20 carry the lowered half squared norm of k_classify's dot-product screen
+                // (seg_internal.cuh), both modes; paper mode also -- point 1 the chord length (Eq. 3), point 2
+                // a 1 when the centroid is stored reversed (an exact end-point tie then picks the caller's
+                // direct orientation, so the result does not depend on the stored order)
                 const bool paper = (flags & SEG_MODE_PAPER) != 0;
-                const float w = paper ? (i == 0 ? clen[(size_t)m] : i == 20 ? (P.flipped[m] ? 1.f : 0.f) : 0.f)
-                                      : (i == 0 || i == 10 || i == 20) ? screen_half_norm_host(c) : 0.f;
+                const float w = (i == 0 || i == 10 || i == 20) ? screen_half_norm_host(c)
+                                : !paper ? 0.f : i == 1 ? clen[(size_t)m] : i == 2 ? (P.flipped[m] ? 1.f : 0.f) : 0.f;
                 tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] = make_float4(c[0], c[1], c[2], w);
                 tiles_cm[((size_t)t * TILE + k) * NPTS + i] = make_float4(c[0], c[1], c[2], 0.f);
                 for (int d = 0; d < 3; ++d) {
