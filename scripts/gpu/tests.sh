@@ -2,5 +2,5 @@
 set -x
 python -c "from paper_1912_11494_b200 import _build; _build.build(force=True)"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?; tail -2 gpurun_out/smoke.log
-timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 grep -E "passed|failed|FAILED|Error" gpurun_out/pytest_gpu.log | head -30
