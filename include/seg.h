@@ -207,6 +207,20 @@ int seg_resample(const float *points, const int64_t *offsets, int64_t N, float *
 int seg_classify_keys(const seg_atlas *atlas, const float *fibers, int64_t N, uint64_t *keys, void *stream);
 int seg_keys_to_labels(const uint64_t *keys, int64_t N, int32_t mode, int32_t *label, float *dist, void *stream);
 
+/*
+ * seg_classify_multi -- row f4's optional half: the original DWM multi-label
+ * assignment the paper replaced by closest-bundle labelling.  For every fiber, bit b of
+ * masks[n * words + b / 32] (bit b % 32) is set iff the bundle's minimum Eq. 2 distance is within its
+ * threshold, D_b <= thr_b; words >= ceil(B / 32) (unused high words are written 0).  The cascade and cull
+ * are the same, cut at each bundle's own threshold (no best-so-far across bundles); the closest-bundle
+ * label of seg_classify is the argmin of D_b over the set bits.  A non-finite fiber gets an all-zero mask.
+ * Exact-mode atlases with B <= 128.  Device pointers only, asynchronous on `stream`.
+ * Errors: SEG_EINVAL (paper-mode atlas, B > 128, words out of range, N out of range, null or misaligned
+ * (4 B) pointers, host memory or another device), SEG_ENOMEM, SEG_ECUDA.
+ */
+int seg_classify_multi(const seg_atlas *atlas, const float *fibers, int64_t N, uint32_t *masks, int32_t words,
+                       void *stream);
+
 /* Shape of a built atlas (for tests and the bench). */
 typedef struct {
     int64_t n_centroids;  /* M */

@@ -67,6 +67,10 @@ def _load():
             for fn in (lib.oracle_classify_sound, lib.oracle_classify_paper_sound):
                 fn.restype = ctypes.c_int
                 fn.argtypes = cls_args
+            lib.oracle_classify_multi.restype = ctypes.c_int
+            lib.oracle_classify_multi.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                                                  ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
             lib.oracle_orientation_ambiguous.restype = ctypes.c_int
             lib.oracle_orientation_ambiguous.argtypes = [f32p, f32p]
             lib.oracle_polyline_length.restype = ctypes.c_double
@@ -208,3 +212,34 @@ def classify(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM,
         else:
             out["lo"], out["hi"] = lo, hi
     return out
+
+
+def classify_multi(fibers, centroids, bundle_id, thresh, delta: float = DELTA_MM, words: int | None = None,
+                   threads: int | None = None):
+    """Multi-label masks (row f4's optional half, PAPER.md:163's original DWM behaviour): bit b of
+    mask[n] set iff D_b(n) <= thr_b; amb[n] marks the bits within delta of the threshold (either value is
+    a correct answer there).  Returns dict(mask uint32[n, words], amb uint32[n, words])."""
+    lib = _load()
+    fib = _f32(fibers).reshape(-1, 21, 3)
+    cen = _f32(centroids).reshape(-1, 21, 3)
+    bid = np.ascontiguousarray(bundle_id, dtype=np.int32)
+    thr = _f32(thresh).reshape(-1)
+    n, m, b = fib.shape[0], cen.shape[0], thr.shape[0]
+    words = words if words is not None else (b + 31) // 32
+    mask = np.zeros((n, words), np.uint32)
+    amb = np.zeros((n, words), np.uint32)
+    threads = max(1, min(threads or os.cpu_count() or 1, max(n, 1)))
+    bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+
+    def run(lo, hi):
+        if hi <= lo:
+            return 0
+        return lib.oracle_classify_multi(fib[lo:].ctypes.data, hi - lo, cen.ctypes.data, bid.ctypes.data, m,
+                                         thr.ctypes.data, b, float(delta), words, mask[lo:].ctypes.data,
+                                         amb[lo:].ctypes.data)
+
+    with ThreadPoolExecutor(threads) as ex:
+        rcs = list(ex.map(lambda i: run(int(bounds[i]), int(bounds[i + 1])), range(threads)))
+    if any(rcs):
+        raise ValueError("oracle_classify_multi: invalid arguments")
+    return dict(mask=mask, amb=amb)

@@ -569,3 +569,49 @@ int oracle_classify_paper_sound(const float *fibers, int64_t n,
     free(S); free(L); free(H); free(cut); free(lc); free(c10);
     return 0;
 }
+
+/* ======================================================================================
+ * Multi-label output (optional half): the original DWM behaviour the
+ * paper replaced by closest-bundle labelling ("... a fiber could be assigned to
+ * several bundles").  Plain definition: per fiber, bit b of the mask is set iff D_b <= thr_b
+ * (D_b = min over the bundle's centroids of Eq. 2's d_ME, as in oracle_classify), B <= 32 * words.
+ * amb (nullable) marks the bits the tie band leaves open: |d_b - thr_b| <= delta.  A non-finite
+ * fiber gets an all-zero mask (reading R12: it is unassigned).
+ * ====================================================================================== */
+int oracle_classify_multi(const float *fibers, int64_t n,
+                          const float *centroids, const int32_t *bundle_id, int64_t M,
+                          const float *thresh, int32_t B, double delta, int32_t words,
+                          uint32_t *mask, uint32_t *amb)
+{
+    if (!bundle_ids_valid(bundle_id, M, B) || words < 1 || B > 32 * words)
+        return -1;
+    double *Db = alloc_doubles(B);
+    if (!Db)
+        return -1;
+    for (int64_t f = 0; f < n; f++) {
+        const float *a = fibers + (size_t)f * 3 * NPTS;
+        uint32_t *mf = mask + (size_t)f * words, *af = amb ? amb + (size_t)f * words : NULL;
+        for (int32_t w = 0; w < words; w++) {
+            mf[w] = 0;
+            if (af) af[w] = 0;
+        }
+        if (!fiber_is_finite(a))
+            continue;
+        for (int32_t b = 0; b < B; b++)
+            Db[b] = INFINITY;
+        for (int64_t m = 0; m < M; m++) {
+            double d2 = oracle_dme_d2(a, centroids + (size_t)m * 3 * NPTS);
+            if (d2 < Db[bundle_id[m]])
+                Db[bundle_id[m]] = d2;
+        }
+        for (int32_t b = 0; b < B; b++) {
+            double t = (double)thresh[b];
+            if (Db[b] <= t * t)
+                mf[b >> 5] |= 1u << (b & 31);
+            if (af && fabs(sqrt(Db[b]) - t) <= delta)
+                af[b >> 5] |= 1u << (b & 31);
+        }
+    }
+    free(Db);
+    return 0;
+}

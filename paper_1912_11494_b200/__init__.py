@@ -141,6 +141,21 @@ class Atlas:
         return keys
 
 
+    def classify_multi(self, fibers, masks=None, stream=None):
+        """Row f4's optional half (seg_classify_multi): every bundle within threshold, the original DWM
+        assignment.  Returns int32 CUDA tensor [N, ceil(B/32)] of bit masks (bit b of word
+        b // 32 = bundle b); exact-mode atlases with B <= 128."""
+        import torch
+        _check_array(fibers, np.float32, (21, 3), "fibers")
+        if not (_is_torch(fibers) and fibers.is_cuda):
+            raise TypeError("fibers: classify_multi takes CUDA tensors")
+        n, words = int(fibers.shape[0]), (self.B + 31) // 32
+        if masks is None:
+            masks = torch.empty((n, words), dtype=torch.int32, device=fibers.device)
+        binding.seg_classify_multi(self._h, fibers, n, masks, int(masks.shape[1]), self._stream(fibers, stream))
+        return masks
+
+
 def group_by_bundle(label, dist, B: int, stream=None):
     """Row f3: the segmented bundles of a classified subject (seg_group_by_bundle).
 

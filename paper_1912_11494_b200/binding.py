@@ -59,6 +59,8 @@ def _load() -> ctypes.CDLL:
     lib.seg_resample.argtypes = [vp, vp, i64, vp, vp]
     lib.seg_classify_keys.restype = ctypes.c_int
     lib.seg_classify_keys.argtypes = [vp, vp, i64, vp, vp]
+    lib.seg_classify_multi.restype = ctypes.c_int
+    lib.seg_classify_multi.argtypes = [vp, vp, i64, vp, i32, vp]
     lib.seg_keys_to_labels.restype = ctypes.c_int
     lib.seg_keys_to_labels.argtypes = [vp, i64, i32, vp, vp, vp]
     lib.seg_classify.restype = ctypes.c_int
@@ -84,7 +86,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 EXPORTS = ("seg_create", "seg_create_ex", "seg_classify", "seg_classify_stats", "seg_get_atlas_info", "seg_plan_tiles",
-           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_resample", "seg_classify_keys", "seg_keys_to_labels", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
+           "seg_profile_enable", "seg_profile_read", "seg_group_by_bundle", "seg_resample", "seg_classify_keys", "seg_classify_multi", "seg_keys_to_labels", "seg_debug_classify_seeded", "seg_destroy", "seg_last_error")
 
 
 def seg_last_error() -> str:
@@ -180,6 +182,10 @@ def seg_resample(points, offsets, N: int, out, stream: int | None = None) -> Non
 
 def seg_classify_keys(atlas: int, fibers, N: int, keys, stream: int | None = None) -> None:
     _check(LIB.seg_classify_keys(atlas, _ptr(fibers), int(N), _ptr(keys), stream))
+
+
+def seg_classify_multi(atlas: int, fibers, N: int, masks, words: int, stream: int | None = None) -> None:
+    _check(LIB.seg_classify_multi(atlas, _ptr(fibers), int(N), _ptr(masks), int(words), stream))
 
 
 def seg_keys_to_labels(keys, N: int, mode: int, label, dist, stream: int | None = None) -> None:

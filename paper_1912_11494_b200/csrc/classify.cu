@@ -518,7 +518,11 @@ __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez,
 #endif
 }
 
-template <bool STATS, bool PAPER>
+// MULTI (row f4's optional half, PAPER.md:163's original DWM assignment): every bundle within its threshold,
+// as a bit mask per fiber (exact mode only).  The cascade is the same with the cutoff thr_b (no best-so-far
+// across bundles), a bundle already accepted for a fiber is skipped, and an accepted candidate ORs its bit.
+constexpr int MULTI_WORDS = 4;          // at most 128 bundles; the masks live in the q2r region (paper-D2 only)
+template <bool STATS, bool PAPER, bool MULTI = false>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemLayout L;
@@ -547,6 +551,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
     float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * PECAP;
     uint16_t *q2e = reinterpret_cast<uint16_t *>(smem + L.q2e) + cw * Q2CAP;
+    // MULTI: this warp's 32 fibers' masks ([32][MULTI_WORDS] words in the otherwise unused q2r region)
+    uint32_t *mmask = reinterpret_cast<uint32_t *>(smem + L.q2r) + cw * 32 * MULTI_WORDS;
+    static_assert(NCW * 32 * MULTI_WORDS * sizeof(uint32_t) <= NCW * Q2CAP * sizeof(float), "masks fit in q2r");
+    auto has_bundle = [&](int f, int b) -> bool { return (mmask[f * MULTI_WORDS + (b >> 5)] >> (b & 31)) & 1u; };
     float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2CAP;
 
     if (threadIdx.x == 0) {
@@ -658,6 +666,10 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             flen[lane] = len;
         }
         best[lane] = (p.seed && inrange) ? p.seed[fidx] : KEY_NONE;
+        if (MULTI) {
+#pragma unroll
+            for (int w = 0; w < MULTI_WORDS; ++w) mmask[lane * MULTI_WORDS + w] = 0u;
+        }
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
     __syncthreads();
@@ -783,7 +795,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float thr2 = reinterpret_cast<const TileHdr *>(estage)->thr2;
                 const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
-                const float taul = fminf(thr2, key_cut2<PAPER>(best[fl]));
+                const float taul = MULTI ? (has_bundle(fl, b) ? -1.f : thr2) : fminf(thr2, key_cut2<PAPER>(best[fl]));
                 if (keep && r <= taul) {  // re-check against the freshest best (best-first pays here)
                     const float4 *cb = T + c + (o ? 20 * TILE : 0);
                     const int st = o ? -TILE : TILE;
@@ -821,6 +833,11 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                                     atomicMin(best + fl, kk);
                                     if (STATS) cnt[ST_UPD]++;
                                 }
+                            }
+                        } else if (MULTI) {
+                            if (r <= thr2) {
+                                atomicOr(mmask + fl * MULTI_WORDS + (b >> 5), 1u << (b & 31));
+                                if (STATS) cnt[ST_UPD]++;
                             }
                         } else if (r <= thr2) {
                             const unsigned long long kk = ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b;
@@ -863,7 +880,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
             const float thr2 = th.thr2;
             long long ts0 = 0;
             if (STATS) ts0 = clock64();
-            const float tau = fminf(thr2, key_cut2<PAPER>(best[lane]));
+            // MULTI: the bundle's own threshold, or nothing once the fiber holds the bundle (tau < 0: the
+            // bound's NaN radius fails every test)
+            const float tau = MULTI ? (has_bundle(lane, th.bundle) ? -1.f : thr2)
+                                    : fminf(thr2, key_cut2<PAPER>(best[lane]));
             constexpr bool D2FORM = SCREEN_OFF || (PAPER && PAPER_D2);
             const float tcmp = D2FORM ? tau : __fmul_rn(tau, 0.5f);   // the screen works at half scale
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
@@ -1029,7 +1049,11 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                 lab = -1;
                 dd = INFINITY;
             }
-            if (p.keys) {
+            if (MULTI) {
+                const bool fin = !isnan(fm[lane].w);
+                for (int w = 0; w < p.mwords; ++w)
+                    p.masks[(size_t)fidx * p.mwords + w] = (fin && w < MULTI_WORDS) ? mmask[lane * MULTI_WORDS + w] : 0u;
+            } else if (p.keys) {
                 // row f4: the raw best key for an atlas-sharded run (all_reduce MIN over the shards);
                 // exchange space: every key < 2^63, NONE = INT64_MAX, non-finite = INT64_MAX - 1
                 p.keys[fidx] = isnan(fm[lane].w) ? KEY_X_NONFINITE : key == KEY_NONE ? KEY_X_NONE : key;
@@ -1287,6 +1311,8 @@ int classify_fibers_per_cta() { return FPC; }
 
 int classify_max_tiles() { return MAX_TILES; }
 
+int classify_multi_max_bundles() { return 32 * MULTI_WORDS; }
+
 size_t cull_bits_words(int n, int T) { return (size_t)((n + FPC - 1) / FPC) * (size_t)(cull_stride(T) / 2); }
 
 // Longest-processing-time-first launch order for k_classify: CTAs sorted by the length of k_cull's tile
@@ -1370,7 +1396,8 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
         kern<<<grid, NTHREADS, smem, s>>>(p);
         return cudaSuccess;
     };
-    if (p.paper) e = stats ? go(k_classify<true, true>) : go(k_classify<false, true>);
+    if (p.masks) e = stats ? go(k_classify<true, false, true>) : go(k_classify<false, false, true>);
+    else if (p.paper) e = stats ? go(k_classify<true, true>) : go(k_classify<false, true>);
     else e = stats ? go(k_classify<true, false>) : go(k_classify<false, false>);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -592,7 +592,7 @@ struct Scratch {
 // Device pointers, asynchronous on s.
 int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, float *dist, cudaStream_t s,
                     unsigned long long *d_stats, const unsigned long long *seed = nullptr,
-                    unsigned long long *keys = nullptr) {
+                    unsigned long long *keys = nullptr, uint32_t *masks = nullptr, int mwords = 0) {
     if (n == 0) return SEG_OK;
     cudaEvent_t *ev = nullptr;
     if (a->prof_n < a->prof_cap) ev = &a->prof_ev[4 * (a->prof_n++)];
@@ -613,10 +613,12 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
     SEG_CUDA(sc.get(&tbits, sizeof(uint32_t) * cull_bits_words(n, a->T)), "seg_classify: scratch allocation");
     ClassifyParams cp{seed, fib, n, perm, lab, dist, a->tiles, a->th, a->ct, a->bh, a->B, a->T, d_stats, tbits, a->paper, keys,
                       nullptr, a->tiles_cm};
+    cp.masks = masks;
+    cp.mwords = mwords;
 #ifndef SEG_NOPAPERSEED
-    {   // k_cull names each fiber's seed candidate, k_classify evaluates it
+    if (!masks) {   // k_cull names each fiber's seed candidate, k_classify evaluates it (no seed for multi-label)
 #else
-    if (!a->paper) {
+    if (!a->paper && !masks) {
 #endif
         SEG_CUDA(sc.get(&cp.seed_code, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
     }
@@ -642,7 +644,7 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
 constexpr int64_t DEV_CHUNK = int64_t(1) << 23;
 int classify_device_sliced(const seg_atlas *a, const float *fib, int64_t N, int32_t *lab, float *dist,
                            cudaStream_t s, unsigned long long *d_stats, const unsigned long long *seed = nullptr,
-                           unsigned long long *keys = nullptr) {
+                           unsigned long long *keys = nullptr, uint32_t *masks = nullptr, int mwords = 0) {
     // SEG_DEV_CHUNK (tests only): a smaller slice, to exercise the slicing at small N
     static const int64_t chunk = [] {
         const char *e = std::getenv("SEG_DEV_CHUNK");
@@ -652,7 +654,8 @@ int classify_device_sliced(const seg_atlas *a, const float *fib, int64_t N, int3
     for (int64_t c0 = 0; c0 < N; c0 += chunk) {
         const int n = (int)std::min<int64_t>(chunk, N - c0);
         const int rc = classify_device(a, fib + c0 * 3 * NPTS, n, lab ? lab + c0 : nullptr, dist ? dist + c0 : nullptr,
-                                       s, d_stats, seed ? seed + c0 : nullptr, keys ? keys + c0 : nullptr);
+                                       s, d_stats, seed ? seed + c0 : nullptr, keys ? keys + c0 : nullptr,
+                                       masks ? masks + c0 * mwords : nullptr, mwords);
         if (rc) return rc;
     }
     return SEG_OK;
@@ -937,6 +940,37 @@ extern "C" int seg_classify_keys(const seg_atlas *a, const float *fibers, int64_
     if (!guard.ok) return fail(SEG_ECUDA, "seg_classify_keys: cudaSetDevice failed");
     const int rc = classify_device_sliced(a, fibers, N, nullptr, nullptr, (cudaStream_t)stream, nullptr, nullptr,
                                           reinterpret_cast<unsigned long long *>(keys));
+    if (!rc) g_err.clear();
+    return rc;
+}
+
+// ----------------------------------------------------------------------------------------
+// seg_classify_multi (row f4's optional half: the original DWM multi-label assignment)
+// ----------------------------------------------------------------------------------------
+extern "C" int seg_classify_multi(const seg_atlas *a, const float *fibers, int64_t N, uint32_t *masks, int32_t words,
+                                  void *stream) {
+    if (!a) return fail(SEG_EINVAL, "seg_classify_multi: null atlas");
+    if (a->paper) return fail(SEG_EINVAL, "seg_classify_multi: exact-mode atlases only");
+    if (a->B > classify_multi_max_bundles())
+        return fail(SEG_EINVAL, "seg_classify_multi: at most " + std::to_string(classify_multi_max_bundles()) + " bundles");
+    if (words < (a->B + 31) / 32 || words > 1024)
+        return fail(SEG_EINVAL, "seg_classify_multi: words must be in [ceil(B / 32), 1024]");
+    if (N < 0 || N > INT32_MAX) return fail(SEG_EINVAL, "seg_classify_multi: N must be in [0, 2^31-1]");
+    if (N == 0) {
+        g_err.clear();
+        return SEG_OK;
+    }
+    if (!fibers || !masks) return fail(SEG_EINVAL, "seg_classify_multi: null pointer with N > 0");
+    if (((uintptr_t)fibers & 3) || ((uintptr_t)masks & 3)) return fail(SEG_EINVAL, "seg_classify_multi: misaligned pointer");
+    int d0 = -1, d1 = -1;
+    const int k0 = pointer_kind(fibers, &d0), k1 = pointer_kind(masks, &d1);
+    if (k0 < 0 || k1 < 0) return fail(SEG_ECUDA, "seg_classify_multi: no usable CUDA device");
+    if (k0 != 1 || k1 != 1 || d0 != a->device || d1 != a->device)
+        return fail(SEG_EINVAL, "seg_classify_multi: device pointers on the atlas's device only");
+    DeviceGuard guard(a->device);
+    if (!guard.ok) return fail(SEG_ECUDA, "seg_classify_multi: cudaSetDevice failed");
+    const int rc = classify_device_sliced(a, fibers, N, nullptr, nullptr, (cudaStream_t)stream, nullptr, nullptr,
+                                          nullptr, masks, words);
     if (!rc) g_err.clear();
     return rc;
 }

@@ -102,6 +102,8 @@ struct ClassifyParams {
     int32_t *seed_code;            // nullable [n] by fiber: k_cull's seed candidate, (tile << 6) | (centroid << 1) | o, -1 = none
     const float4 *tiles_cm;        // [T][32][21] centroid-major copy of the tile points (the seed evaluation)
     int32_t *cta_order = nullptr;  // nullable [grid]: k_classify's CTA i works on fiber window cta_order[i]
+    uint32_t *masks = nullptr;     // nullable [n][mwords]: multi-label output (row f4), bit b = bundle b within threshold
+    int mwords = 0;
 };
 
 struct MortonParams {
@@ -148,6 +150,7 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
 size_t classify_smem_bytes(int B, int T);
 size_t cull_bits_words(int n, int T);
 int classify_max_tiles();
+int classify_multi_max_bundles();
 int classify_fibers_per_cta();
 cudaError_t launch_group(GroupParams p, cudaStream_t s);
 size_t group_scratch_words(int64_t n, int B);

@@ -75,3 +75,12 @@ for world in (2, 4, 8):
                           unsharded_ms=full_ms, shard_ms=per, max_shard_ms=max(per), sum_shard_ms=sum(per),
                           strong_scaling_speedup=full_ms / max(per), min_decode_equals_unsharded=same)))
 
+
+# row f4's optional half: the multi-label (DWM) masks, every bundle within threshold (seg_classify_multi)
+masks = torch.empty((N, (at.B + 31) // 32), dtype=torch.int32, device="cuda")
+ms = timeit(lambda: A.classify_multi(fib, masks), reps=10)
+m64 = masks.to(torch.int64)
+nmulti = int((sum((m64 >> k) & 1 for k in range(32)).sum(-1) > 1).sum())
+print(json.dumps(dict(row="f4 multi-label seg_classify_multi", config=f"cfg{cfg}, {N:,} fibers x {at.M:,} centroids",
+                      ms=ms, comparisons_per_s=N * at.M / (ms * 1e-3), fibers_per_s=N / (ms * 1e-3),
+                      single_label_ms=full_ms, fibers_with_several_bundles=nmulti)))
