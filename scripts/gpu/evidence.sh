@@ -10,3 +10,4 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 python scripts/bench_brief.py gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
 timeout 1500 python scripts/report.py > gpurun_out/report_rows.jsonl 2> gpurun_out/report.err; echo report_rc=$?
+timeout 900 python scripts/bench_rows.py 3 > gpurun_out/bench_rows.jsonl 2> gpurun_out/bench_rows.err; echo rows_rc=$?
