@@ -439,6 +439,7 @@ struct SmemLayout {
         ring = o; o += (size_t)STAGES * TILE_STRIDE_BYTES;
         fxy = o;  o += (size_t)NCW * NMID * PP * sizeof(float2);
         fz = o;   o += (size_t)NCW * NMID * PP * sizeof(float);
+        o = (o + 15) & ~(size_t)15;   // the float4 / u64 arrays below need 16-B alignment whatever NCW and PP are
         // fe / fm / fez 16 B apart in bank alignment, so the ingest's writes of x0, x10, z0 (etc.) of one
         // fiber do not share a bank (bank model: 3.3 -> 2.3 wavefronts per ingest instruction)
         fe = o;   o += (size_t)FPC * sizeof(float4) + SEG_PLANE_SKEW;   // (x0, x20, y0, y20)
@@ -458,6 +459,8 @@ struct SmemLayout {
 
 // CTAS_PER_SM CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
 static_assert(SmemLayout().total <= 233472 / CTAS_PER_SM - 1024, "k_classify shared memory exceeds the CTA/SM budget");
+static_assert(SmemLayout().fe % 16 == 0 && SmemLayout().fm % 16 == 0 && SmemLayout().fez % 16 == 0 &&
+              SmemLayout().best % 8 == 0 && SmemLayout().bars % 8 == 0, "k_classify shared-memory arrays misaligned");
 
 // plane slot of fiber point i (i != 0, 10, 20)
 __host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
