@@ -139,7 +139,7 @@ def run_reference(args):
     v = statistics.median([r["value"] for r in vals])
     line = dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * statistics.median([r["seconds"] for r in vals]),
-                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                higher_is_better=True, scaling=args.scaling, vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=workload_name(args.config, args.mode), sample=vals[-1]["sample"]),
                 fibers_per_s=statistics.median([r["fibers_per_s"] for r in vals]),
                 cpu_baseline=dict(value=v, unit=UNIT, cores=vals[-1]["cores"], kind="oracle",
@@ -444,7 +444,8 @@ def main():
             vs_baseline=None, dtype="f32", data="synthetic",
             config=dict(workload=workload_name(cfg, args.mode), fibers=n_job, fibers_per_gpu=N,
                         centroids=spec["n_centroids"], bundles=spec["n_bundles"],
-                        parallelism=(f"one subject sharded contiguously over {world} ranks (atlas NCCL-broadcast, "
+                        parallelism=("one GPU, the whole subject" if world == 1 else
+                                     f"one subject sharded contiguously over {world} ranks (atlas NCCL-broadcast, "
                                      + ("results stored into rank 0 by each rank's kernel epilogue over NVLink "
                                         "(fused gather)" if peer is not None else "results all_gathered (NCCL)")
                                      + " in every step)" if strong else
