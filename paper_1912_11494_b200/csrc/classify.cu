@@ -386,6 +386,9 @@ constexpr int CULL_UNROLL = SEG_CULL_UNROLL;     // k_cull's 32-tile chunk loop
 #endif
 constexpr int RANK_UNROLL = SEG_RANK_UNROLL;     // k_cull's best-first ranking loop
 constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
+#ifndef SEG_VOTE_JJ_ALWAYS
+#define SEG_VOTE_JJ_ALWAYS 0
+#endif
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
 // the dot-product screen: 1 since round 2's bank-conflict and branch fixes (cfg 3 -1.1%, cfg 4 -1.6% vs 2;
 // 3: +1.5%); round 1 had measured 2 best.  Paper mode, d2 form, with the per-fiber VOTE: 2 (1: +0.9%).
@@ -973,7 +976,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         tjv[q] = tj;
                         // one VOTE.ANY per fiber: far shorter latency than a REDUX.OR of the step's bits
                         // (cfg 3: -3.6%)
-                        if (__any_sync(0xffffffffu, jj[q] >= 0 && fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
+                        // one fiber per step: the loop runs while pm != 0, so the slot is never empty (no
+                        // jj >= 0 test on the vote's dependent chain)
+                        const bool live = (FB == 1 && !SEG_VOTE_JJ_ALWAYS) || jj[q] >= 0;
+                        if (__any_sync(0xffffffffu, live && fminf(rdv[q], riv[q]) <= tj)) hit |= 1u << q;
                         if (STATS && jj[q] >= 0 && m10 <= tj) { cnt[ST_T2]++; cnt[ST_PDIST] += 4; }
                     }
 #if defined(SEG_EXP) && SEG_EXP == 3
