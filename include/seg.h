@@ -139,10 +139,10 @@ int seg_classify(const seg_atlas *atlas, const float *fibers, int64_t N,
  *   [9] lane point-distance evaluations (Eq. 1, all stages and the bounds)
  *   [10] lane tile-bound tests (live, boxes)         [11] CTAs
  *   clock64 cycles summed over consumer warps: [12] tile loop, [13] waiting for a tile,
- *   [14] best-first candidate selection (incl. the candidate rounds it triggers),
+ *   [14] candidate selection (stack pushes, incl. the overflow rounds they trigger),
  *   [15] candidate rounds, [16] live tile-bound test, [17] fiber ingest (start -> first barrier)
  *   [18] candidate rounds run, [19] candidate lanes over those rounds, [20] fibers with a surviving
- *   orientation after test2 in a tile (best-first selections), [21] of [18]: winners' rounds
+ *   orientation after test2 in a tile (stack pushes), [21] reserved (0)
  * A separate kernel instantiation; it computes the same labels and distances.
  */
 int seg_classify_stats(const seg_atlas *atlas, const float *fibers, int64_t N,

@@ -20,7 +20,7 @@ STAT_NAMES = ("fibers", "warp_tiles_listed", "warp_tiles_computed", "lane_tile_p
               "lane_test2", "lane_test34", "lane_full21", "best_updates", "lane_point_dists",
               "lane_bound_tests", "ctas",
               "cyc_consumer", "cyc_full_wait", "cyc_hit_select", "cyc_cand_rounds", "cyc_tile_test", "cyc_ingest",
-              "rounds", "round_lanes", "hit_fibers", "winner_rounds")
+              "rounds", "round_lanes", "hit_fibers", "reserved21")
 
 
 class SegError(RuntimeError):

@@ -10,7 +10,7 @@
 //        streamed into a shared-memory ring by 1-D TMA bulk copies from a producer warp; per tile the
 //        exact sphere bound with each fiber's live cutoff decided by warp ballot (a2), then the
 //        paper's cascade with lane = centroid: test1 centre point (a3), test2 end points in both
-//        orientations (a4), best-first candidate rounds with test3 four points (a5) and test4 the
+//        orientations (a4), candidate rounds with test3 four points (a5) and test4 the
 //        rest with early exits (a6), the closest-bundle key update (a7,
 //        PAPER.md:129-133, :163) and the epilogue scattered back through the permutation (a8,
 //        PAPER.md:138).  DESIGN.md Sec. 5 has the layout, the roofline and the measurements.
@@ -341,14 +341,14 @@ size_t morton_scratch_words(int bits) {
 //   a2  the PRODUCER warp streams the tile list k_cull wrote for this CTA through a STAGES-deep ring
 //       (one 1-D TMA bulk copy per tile, cp.async.bulk -> UBLKCP, mbarrier completion); an end
 //       marker closes the stream.  Each consumer lane re-tests its fiber against the tile's three
-//       spheres with its live cutoff tau = min(thr_b^2, best^2); a warp ballot picks the fibers.
+//       boxes with its live cutoff tau = min(thr_b^2, best^2); a warp ballot picks the fibers.
 //   a3+a4  consumers, dense and transposed: lane c holds centroid c's points 0/10/20, the warp walks
-//       its passing fibers 4 at a time: test1 (centre point) and test2 (end points, both
+//       its passing fibers one at a time: test1 (centre point) and test2 (end points, both
 //       orientations, FFMA2) for all 32 centroids at once;
-//   a5+a6  best-first: per fiber the alive orientation with the smallest 3-point score is its winner
-//       (a winners' round first), every other alive orientation goes to a candidate stack that is
-//       re-checked against the freshest best; test3 = points {3,17,7,13}, test4 = the rest with an
-//       early exit after every group;
+//   a5+a6  every alive orientation goes onto the warp's candidate stack; at the end of the tile the
+//       stack runs in rounds of 32 lanes, each entry re-checked against its fiber's freshest best;
+//       test3 = points {3,17,7,13}, test4 = the rest with an early exit after every group
+//       (PAPER.md:159);
 //   a7  a finished orientation updates its fiber's best (d^2, bundle) key -- paper mode:
 //       (d_ME + TN, bundle) -- with a shared-memory 64-bit atomicMin (lexicographic, so tile order
 //       and orientation never matter);
@@ -362,10 +362,23 @@ constexpr int NCW = SEG_NCW;           // consumer warps (4 warps x 3 CTAs/SM me
 constexpr int CTAS_PER_SM = 2;
 constexpr int FPC = NCW * 32;          // fibers per CTA
 constexpr int NTHREADS = FPC + 32;     // + producer warp
+#ifndef SEG_EARLY_TMA
+#define SEG_EARLY_TMA 1   // the first STAGES tile copies issued before the fiber ingest
+#endif
 #ifndef SEG_STAGES
 #define SEG_STAGES 3
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
+#ifndef SEG_DEFER_BELOW
+#define SEG_DEFER_BELOW 32
+#endif
+#ifndef SEG_DEFER_TILES
+#define SEG_DEFER_TILES 1
+#endif
+// candidate stacks shorter than DEFER_BELOW entries are carried over to the next tile, holding at most
+// DEFER_TILES ring stages (< STAGES - 1 so the producer keeps a tile of lookahead); 0 = flush every tile
+constexpr int DEFER_BELOW = SEG_DEFER_BELOW, DEFER_TILES = SEG_DEFER_TILES;
+static_assert(DEFER_TILES >= 0 && DEFER_TILES <= STAGES - 1, "a warp must not hold every ring stage");
 #ifndef SEG_CULL_UNROLL
 #define SEG_CULL_UNROLL 32
 #endif
@@ -414,7 +427,6 @@ constexpr int PP = SEG_PLANE_PITCH;
 #define SEG_Q2CAP 184
 #endif
 constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (184: room for the plane pitch)
-constexpr int PECAP = 32;              // winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
 constexpr unsigned long long KEY_X_NONE = 0x7fffffffffffffffull;       // seg.h SEG_KEY_NONE
@@ -427,7 +439,7 @@ constexpr int MAX_SMEM_BUNDLES = 512;  // k_cull stages up to this many bundle h
 
 enum {
     ST_FIBERS = 0, ST_WT_LISTED, ST_WT_COMPUTED, ST_LT_PASS, ST_T1, ST_T2, ST_T34, ST_FULL, ST_UPD,
-    ST_PDIST, ST_SPHERE, ST_CTAS, ST_CYC_CONS, ST_CYC_FULLWAIT, ST_CYC_HIT, ST_CYC_FLUSH, ST_CYC_SPHERE, ST_CYC_INGEST, ST_ROUNDS, ST_ROUND_LANES, ST_HITS, ST_ROUND_WIN, ST_N
+    ST_PDIST, ST_SPHERE, ST_CTAS, ST_CYC_CONS, ST_CYC_FULLWAIT, ST_CYC_HIT, ST_CYC_FLUSH, ST_CYC_SPHERE, ST_CYC_INGEST, ST_ROUNDS, ST_ROUND_LANES, ST_HITS, ST_RESERVED21, ST_N
 };
 
 struct StageMeta {
@@ -435,7 +447,7 @@ struct StageMeta {
 };
 
 struct SmemLayout {
-    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, pe = 0, pr = 0, q2e = 0, q2r = 0, best = 0, flen = 0,
+    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, q2e = 0, q2r = 0, best = 0, flen = 0,
            bars = 0, meta = 0, total = 0;
     __host__ __device__ constexpr SmemLayout() {
         size_t o = 0;
@@ -451,9 +463,7 @@ struct SmemLayout {
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
         flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
-        pr = o;   o += (size_t)NCW * PECAP * sizeof(float);
         q2r = o;  o += (size_t)NCW * Q2CAP * sizeof(float);
-        pe = o;   o += (size_t)NCW * PECAP * sizeof(uint16_t);
         q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint16_t);
         meta = o; o += (size_t)STAGES * sizeof(StageMeta);
         total = (o + 127) & ~(size_t)127;
@@ -554,21 +564,39 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     float4 *fez = fez_all + cw * 32;
     unsigned long long *best = best_all + cw * 32;
     float *flen = reinterpret_cast<float *>(smem + L.flen) + cw * 32;
-    uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
-    float *pr = reinterpret_cast<float *>(smem + L.pr) + cw * PECAP;
-    uint16_t *q2e = reinterpret_cast<uint16_t *>(smem + L.q2e) + cw * Q2CAP;
+    uint16_t *q2e = reinterpret_cast<uint16_t *>(smem + L.q2e) + cw * Q2CAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
     // MULTI: this warp's 32 fibers' masks ([32][MULTI_WORDS] words in the otherwise unused q2r region)
     uint32_t *mmask = reinterpret_cast<uint32_t *>(smem + L.q2r) + cw * 32 * MULTI_WORDS;
     static_assert(NCW * 32 * MULTI_WORDS * sizeof(uint32_t) <= NCW * Q2CAP * sizeof(float), "masks fit in q2r");
     auto has_bundle = [&](int f, int b) -> bool { return (mmask[f * MULTI_WORDS + (b >> 5)] >> (b & 31)) & 1u; };
     float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2CAP;
 
-    if (threadIdx.x == 0) {
+    // the producer lane sets up the ring and issues the first STAGES tile copies (or the end marker) at once,
+    // so they land while the consumers ingest their fibers; the loop below continues from kpre
+    const unsigned short *lst_g = reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)cta * cull_stride(p.T);
+    int kpre = 0, nlist = 0;
+    if (threadIdx.x == FPC) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        nlist = __ldg(lst_g);
+        SEG_DCHECK(nlist >= 0 && nlist <= p.T);
+#if SEG_EARLY_TMA
+        for (; kpre < STAGES && kpre <= nlist; ++kpre) {
+            if (kpre < nlist) {
+                const int t = __ldg(lst_g + 1 + kpre);
+                SEG_DCHECK(t >= 0 && t < p.T);
+                meta[kpre].tile = t;
+                mbar_arrive_expect_tx(full + kpre, TILE_STRIDE_BYTES);
+                bulk_g2s(ring + kpre * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES, full + kpre);
+            } else {
+                meta[kpre].tile = -1;   // end of stream
+                mbar_arrive(full + kpre);
+            }
+        }
+#endif
     }
     unsigned long long cnt[ST_N];
     long long ti0 = 0;
@@ -731,11 +759,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     if (!consumer) {
         // ---- producer warp: stream the tiles k_cull listed for this CTA (TMA bulk copies) ----
         if (lane == 0) {
-            const unsigned short *lst_g =
-                reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)cta * cull_stride(p.T);
-            const int nlist = __ldg(lst_g);
-            SEG_DCHECK(nlist >= 0 && nlist <= p.T);
-            int k = 0;
+            int k = kpre;
             for (; k < nlist; ++k) {
                 const int t = __ldg(lst_g + 1 + k);
                 SEG_DCHECK(t >= 0 && t < p.T);
@@ -745,10 +769,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 mbar_arrive_expect_tx(full + s, TILE_STRIDE_BYTES);
                 bulk_g2s(ring + s * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES, full + s);
             }
-            const int s = k % STAGES, u = k / STAGES;   // end of stream
-            if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
-            meta[s].tile = -1;
-            mbar_arrive(full + s);
+            if (kpre <= nlist) {   // end of stream, unless it went out with the first copies
+                const int s = k % STAGES, u = k / STAGES;
+                if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
+                meta[s].tile = -1;
+                mbar_arrive(full + s);
+            }
         }
     } else {
         // ---- consumers ----
@@ -758,10 +784,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         const bool myok = !isnan(myF10.w);
         // candidate round: full Eq. 2 maximum for one orientation of (fiber fl, centroid c),
         // starting from its 3-point running max r
-        // excl: the round's entries are distinct fibers (a winners' round: at most one winner per
-        // fiber per tile), so the best key is updated by a plain compare-and-store, not an atomic
-        auto run_cand = [&](const uint16_t *qe, const float *qr, int n, bool excl) {
-            if (STATS && lane == 0 && n > 0) { cnt[ST_ROUNDS]++; cnt[ST_ROUND_LANES] += n; if (qe >= pe && qe < pe + PECAP) cnt[ST_ROUND_WIN]++; }
+        // (a fiber may hold several lanes of a round: its best key is updated with a shared-memory atomicMin)
+        auto run_cand = [&](const uint16_t *qe, const float *qr, int n) {
+            if (STATS && lane == 0 && n > 0) { cnt[ST_ROUNDS]++; cnt[ST_ROUND_LANES] += n; }
 #if defined(SEG_EXP) && SEG_EXP == 2
             n = 0;  // experiment: no candidate rounds
 #endif
@@ -802,7 +827,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
                 const float taul = MULTI ? (has_bundle(fl, b) ? -1.f : thr2) : fminf(thr2, key_cut2<PAPER>(best[fl]));
-                if (keep && r <= taul) {  // re-check against the freshest best (best-first pays here)
+                if (keep && r <= taul) {  // re-check against the freshest best (an earlier round of this tile may have lowered it)
                     const float4 *cb = T + c + (o ? 20 * TILE : 0);
                     const int st = o ? -TILE : TILE;
                     bool done = false;
@@ -835,7 +860,6 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                                 const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[W_LEN * TILE + c].w));
                                 if (sc <= thr) {
                                     const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b;
-                                    if (excl) { if (kk < best[fl]) best[fl] = kk; } else
                                     atomicMin(best + fl, kk);
                                     if (STATS) cnt[ST_UPD]++;
                                 }
@@ -847,7 +871,6 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                             }
                         } else if (r <= thr2) {
                             const unsigned long long kk = ((unsigned long long)__float_as_uint(r) << 32) | (uint32_t)b;
-                            if (excl) { if (kk < best[fl]) best[fl] = kk; } else
                             atomicMin(best + fl, kk);
                             if (STATS) cnt[ST_UPD]++;
                         }
@@ -857,18 +880,16 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
             }
             __syncwarp();
         };
-        int np = 0, n2 = 0;
-        auto flush = [&](int keep) {   // best-first: the per-fiber winners, then the rest
+        int n2 = 0;
+        uint32_t pend = 0;   // ring stages (bits) whose candidates still wait on the stack
+        auto flush = [&](int keep) {   // rounds of 32 off the top of the stack until at most `keep` are left
             long long tf0 = 0;
             if (STATS) tf0 = clock64();
             __syncwarp();
-            SEG_DCHECK(np <= 32);
-            if (np > 0) run_cand(pe, pr, np, true);
-            np = 0;
             while (n2 > keep) {
                 const int m = n2 >= 32 ? 32 : n2;
                 n2 -= m;
-                run_cand(q2e + n2, q2r + n2, m, false);
+                run_cand(q2e + n2, q2r + n2, m);
             }
             if (STATS && lane == 0) cnt[ST_CYC_FLUSH] += clock64() - tf0;
         };
@@ -998,34 +1019,18 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         for (int t = 1; t < FB; ++t)
                             if (q == t) { j = jj[t]; rd = rdv[t]; ri = riv[t]; tj = tjv[t]; }
                         const bool ad = rd <= tj, ai = ri <= tj;
-                        // best-first: the centroid with the smallest 3-point score goes to the
-                        // winners' round, every other surviving orientation to q2
-                        float sc = fminf(ad ? rd : INFINITY, ai ? ri : INFINITY);
-                        // the winner's orientation, chosen before the clamp below (a clamped negative
-                        // screen value would no longer compare equal to rd)
-                        const int wo = (ad && (!ai || rd <= ri)) ? 0 : 1;
-                        if (!D2FORM) sc = fmaxf(sc, 0.f);   // screen values may be < 0; keep the key order
-                        // the lane rides in the score's 5 low mantissa bits: REDUX.MIN names the winner
-                        // directly (a heuristic choice; every survivor is still evaluated)
-                        const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
-                        const int wl = (int)(smin & 31u);
-                        const bool win = lane == wl;
+                        // every surviving orientation goes onto the candidate stack.  (Round 1 sent each fiber's
+                        // best 3-point survivor to a winners' round first, for its fresher cutoff: one more round
+                        // per tile, which costs more than its pruning saves -- DESIGN.md Sec. 5)
                         if (STATS && lane == 0) cnt[ST_HITS]++;
                         const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
-                        SEG_DCHECK(np < PECAP && j >= 0 && j < 32);
-                        if (win) {
-                            pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
-                            if (PAPER && PAPER_D2) pr[np] = sc;   // otherwise the round re-evaluates the 3 points
-                        }
-                        ++np;
-                        const bool qd = ad && !(win && wo == 0), qi = ai && !(win && wo == 1);
-                        const uint32_t bd = __ballot_sync(0xffffffffu, qd), bi = __ballot_sync(0xffffffffu, qi);
-                        if (qd) {
+                        const uint32_t bd = __ballot_sync(0xffffffffu, ad), bi = __ballot_sync(0xffffffffu, ai);
+                        if (ad) {
                             const int pos = n2 + __popc(bd & lt_mask);
                             q2e[pos] = (uint16_t)e;
                             if (PAPER && PAPER_D2) q2r[pos] = rd;
                         }
-                        if (qi) {
+                        if (ai) {
                             const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
                             q2e[pos] = (uint16_t)(e | (1u << 10));
                             if (PAPER && PAPER_D2) q2r[pos] = ri;
@@ -1037,10 +1042,21 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                     if (STATS && lane == 0) cnt[ST_CYC_HIT] += clock64() - th0;
                 }
             }
+            // a stack shorter than one round waits for the next tile's entries (its stage stays held, at most
+            // DEFER_TILES of them: the producer refills a stage only after every warp released it, and this
+            // warp's next tile must not depend on a stage it holds itself)
+            if (n2 > 0 && n2 < DEFER_BELOW && __popc(pend) < DEFER_TILES) {
+                pend |= 1u << s;
+                continue;
+            }
             flush(0);
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);
+            pend |= 1u << s;
+            if (lane == 0)
+                for (uint32_t b = pend; b; b &= b - 1) mbar_arrive(empty + (__ffs(b) - 1));
+            pend = 0;
         }
+        if (pend) flush(0);
 
         if (STATS && lane == 0) cnt[ST_CYC_CONS] += clock64() - tc0;
         // ---- a8: epilogue ----

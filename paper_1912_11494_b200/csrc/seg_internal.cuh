@@ -21,7 +21,7 @@ constexpr int TILE = 32;                 // centroids per tile (one bit per cent
 constexpr int TILE_F4 = NPTS * TILE;     // float4 of tile point data: [21 points][32 centroids]
 constexpr int TILE_HDR_F4 = 7;           // the tile's 112-B TileHdr travels in front of its data
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
-constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,816 B -> one 1-D TMA bulk copy
+constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,864 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
 
 // Exact mode's dot-product screen for test1 / test2.  Each squared distance of the
