@@ -1169,6 +1169,11 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
             const bool bpass = d2(F10.x, F10.y, F10.z, c) <= c.w;
             if (!__any_sync(0xffffffffu, bpass)) continue;
             const BundleHdr h = p.bh[b];
+#if defined(SEG_EXP) && SEG_EXP == 5
+            // experiment: every tile of a passing bundle listed, no per-fiber tile tests
+            for (int t = h.t0 + lane; t < h.t1; t += 32) atomicOr(tb + (t >> 5), 1u << (t & 31));
+            if (h.t1 > 0) continue;
+#endif
             for (int t0 = h.t0; t0 < h.t1; t0 += 32) {
                 // 32 tiles per chunk: independent header loads and tests (ILP)
                 const int nt = min(32, h.t1 - t0);
@@ -1219,6 +1224,10 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
         const int myfidx = gi < p.n ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
         const bool want = myfidx >= 0 && ntile >= 0;
         if (myfidx >= 0 && !want) p.seed_code[myfidx] = -1;
+#if defined(SEG_EXP) && (SEG_EXP == 4 || SEG_EXP == 5)
+        if (want) p.seed_code[myfidx] = -1;   // experiment: no seeds
+        if (p.n >= 0) goto seed_done;
+#endif
         int ct = -1;
         float thr2 = 0.f;
         float4 c10 = make_float4(0.f, 0.f, 0.f, 0.f), c0 = c10, c20 = c10;
@@ -1255,6 +1264,9 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
             if (lane == 0) p.seed_code[fj] = code;
         }
     }
+#if defined(SEG_EXP) && (SEG_EXP == 4 || SEG_EXP == 5)
+seed_done:
+#endif
     __syncthreads();
     // the CTA's tiles from the bit set (warp 0: prefix over the words), in tile order
     if (threadIdx.x < 32) {
