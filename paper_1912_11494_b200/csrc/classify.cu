@@ -427,6 +427,7 @@ constexpr int PP = SEG_PLANE_PITCH;
 #define SEG_Q2CAP 184
 #endif
 constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (184: room for the plane pitch)
+constexpr int PECAP = 32;              // MULTI: winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
 constexpr unsigned long long KEY_X_NONE = 0x7fffffffffffffffull;       // seg.h SEG_KEY_NONE
@@ -447,7 +448,7 @@ struct StageMeta {
 };
 
 struct SmemLayout {
-    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, q2e = 0, q2r = 0, best = 0, flen = 0,
+    size_t ring = 0, fxy = 0, fz = 0, fe = 0, fez = 0, fm = 0, q2e = 0, q2r = 0, pe = 0, best = 0, flen = 0,
            bars = 0, meta = 0, total = 0;
     __host__ __device__ constexpr SmemLayout() {
         size_t o = 0;
@@ -465,6 +466,7 @@ struct SmemLayout {
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
         q2r = o;  o += (size_t)NCW * Q2CAP * sizeof(float);
         q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint16_t);
+        pe = o;   o += (size_t)NCW * PECAP * sizeof(uint16_t);
         meta = o; o += (size_t)STAGES * sizeof(StageMeta);
         total = (o + 127) & ~(size_t)127;
     }
@@ -565,6 +567,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     unsigned long long *best = best_all + cw * 32;
     float *flen = reinterpret_cast<float *>(smem + L.flen) + cw * 32;
     uint16_t *q2e = reinterpret_cast<uint16_t *>(smem + L.q2e) + cw * Q2CAP;   // entries: c | fiber << 5 | o << 10 | stage << 11
+    uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;     // MULTI: the tile's winners, same format
     // MULTI: this warp's 32 fibers' masks ([32][MULTI_WORDS] words in the otherwise unused q2r region)
     uint32_t *mmask = reinterpret_cast<uint32_t *>(smem + L.q2r) + cw * 32 * MULTI_WORDS;
     static_assert(NCW * 32 * MULTI_WORDS * sizeof(uint32_t) <= NCW * Q2CAP * sizeof(float), "masks fit in q2r");
@@ -880,12 +883,14 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
             }
             __syncwarp();
         };
-        int n2 = 0;
+        int n2 = 0, np = 0;
         uint32_t pend = 0;   // ring stages (bits) whose candidates still wait on the stack
         auto flush = [&](int keep) {   // rounds of 32 off the top of the stack until at most `keep` are left
             long long tf0 = 0;
             if (STATS) tf0 = clock64();
             __syncwarp();
+            if (MULTI && np > 0) run_cand(pe, q2r, np);   // MULTI: the winners first (q2r unused: no PAPER_D2)
+            np = 0;
             while (n2 > keep) {
                 const int m = n2 >= 32 ? 32 : n2;
                 n2 -= m;
@@ -1024,13 +1029,28 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         // per tile, which costs more than its pruning saves -- DESIGN.md Sec. 5)
                         if (STATS && lane == 0) cnt[ST_HITS]++;
                         const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
-                        const uint32_t bd = __ballot_sync(0xffffffffu, ad), bi = __ballot_sync(0xffffffffu, ai);
-                        if (ad) {
+                        bool qd = ad, qi = ai;
+                        if (MULTI) {
+                            // multi-label masks keep a winners' round: one accepted centroid settles the bundle
+                            // for the fiber, so the tile's other candidates of that fiber stop at their re-check.
+                            // The winner is the smallest screened 3-point score (lane in the 5 low bits)
+                            const float sc = fmaxf(fminf(ad ? rd : INFINITY, ai ? ri : INFINITY), 0.f);
+                            const int wo = (ad && (!ai || rd <= ri)) ? 0 : 1;
+                            const uint32_t smin = __reduce_min_sync(0xffffffffu, (__float_as_uint(sc) & ~31u) | (uint32_t)lane);
+                            const bool win = lane == (int)(smin & 31u);
+                            SEG_DCHECK(np < PECAP);
+                            if (win) pe[np] = (uint16_t)(e | ((uint32_t)wo << 10));
+                            ++np;
+                            qd = ad && !(win && wo == 0);
+                            qi = ai && !(win && wo == 1);
+                        }
+                        const uint32_t bd = __ballot_sync(0xffffffffu, qd), bi = __ballot_sync(0xffffffffu, qi);
+                        if (qd) {
                             const int pos = n2 + __popc(bd & lt_mask);
                             q2e[pos] = (uint16_t)e;
                             if (PAPER && PAPER_D2) q2r[pos] = rd;
                         }
-                        if (ai) {
+                        if (qi) {
                             const int pos = n2 + __popc(bd) + __popc(bi & lt_mask);
                             q2e[pos] = (uint16_t)(e | (1u << 10));
                             if (PAPER && PAPER_D2) q2r[pos] = ri;
@@ -1045,7 +1065,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
             // a stack shorter than one round waits for the next tile's entries (its stage stays held, at most
             // DEFER_TILES of them: the producer refills a stage only after every warp released it, and this
             // warp's next tile must not depend on a stage it holds itself)
-            if (n2 > 0 && n2 < DEFER_BELOW && __popc(pend) < DEFER_TILES) {
+            if (!MULTI && n2 > 0 && n2 < DEFER_BELOW && __popc(pend) < DEFER_TILES) {
                 pend |= 1u << s;
                 continue;
             }
