@@ -133,9 +133,9 @@ constexpr bool PAPER_D2 = true;
 #else
 constexpr bool PAPER_D2 = false;
 #endif
-// the tile image's w slots (seg_create): 0 / 10 / 20 the screen's half norms; paper mode: 1 the centroid's
-// chord length, 2 the stored-reversed flag
-constexpr int W_LEN = 1, W_FLIP = 2;
+// the tile image (seg_internal.cuh, TI_*): points 0 / 10 / 20 carry the screen's half norms in w; paper mode
+// also fills the per-centroid chord length and stored-reversed flag
+
 // Exact mode's dot-product screen (seg_internal.cuh): h = (s + ...) - a.c for the two fiber points packed
 // in (px, py, pz) against the scalar centroid point q, s = the packed sums of the lowered half norms.
 // Never above d2 / 2 (see there).
@@ -366,14 +366,14 @@ constexpr int NTHREADS = FPC + 32;     // + producer warp
 #define SEG_EARLY_TMA 1   // the first STAGES tile copies issued before the fiber ingest
 #endif
 #ifndef SEG_STAGES
-#define SEG_STAGES 3
+#define SEG_STAGES 4
 #endif
 constexpr int STAGES = SEG_STAGES;     // tile ring depth
 #ifndef SEG_DEFER_BELOW
 #define SEG_DEFER_BELOW 32
 #endif
 #ifndef SEG_DEFER_TILES
-#define SEG_DEFER_TILES 1
+#define SEG_DEFER_TILES 2
 #endif
 // candidate stacks shorter than DEFER_BELOW entries are carried over to the next tile, holding at most
 // DEFER_TILES ring stages (< STAGES - 1 so the producer keeps a tile of lookahead); 0 = flush every tile
@@ -424,9 +424,9 @@ constexpr int PP = SEG_PLANE_PITCH;
 #define SEG_PLANE_SKEW 16
 #endif
 #ifndef SEG_Q2CAP
-#define SEG_Q2CAP 184
+#define SEG_Q2CAP 128
 #endif
-constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (184: room for the plane pitch)
+constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (128: room for the 4th ring stage)
 constexpr int PECAP = 32;              // MULTI: winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
 constexpr unsigned long long KEY_NONE = ~0ull;
@@ -477,8 +477,6 @@ static_assert(SmemLayout().total <= 233472 / CTAS_PER_SM - 1024, "k_classify sha
 static_assert(SmemLayout().fe % 16 == 0 && SmemLayout().fm % 16 == 0 && SmemLayout().fez % 16 == 0 &&
               SmemLayout().best % 8 == 0 && SmemLayout().bars % 8 == 0, "k_classify shared-memory arrays misaligned");
 
-// plane slot of fiber point i (i != 0, 10, 20)
-__host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
 
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
@@ -729,7 +727,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float4 c0p = __ldg(cc), c20p = __ldg(cc + NPTS - 1);
                 const float e00 = d2(E.x, E.z, Ez.x, c0p), e2020 = d2(E.y, E.w, Ez.y, c20p);
                 const float e020 = d2(E.x, E.z, Ez.x, c20p), e200 = d2(E.y, E.w, Ez.y, c0p);
-                const float flip = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + W_FLIP * TILE + c).w;
+                const float flip = __ldg(reinterpret_cast<const float *>(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4) + TI_FLIP + c);
                 const float mi = fmaxf(e020, e200), md = fmaxf(e00, e2020);
                 o = (mi < md || (mi == md && flip != 0.f)) ? 1 : 0;
             }
@@ -744,7 +742,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             }
             if (PAPER) {
                 // score = d_ME + TN (Eq. 3), the lengths as the candidate rounds take them
-                const float clen = __ldg(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4 + W_LEN * TILE + c).w;
+                const float clen = __ldg(reinterpret_cast<const float *>(p.tiles + (size_t)tn * TILE_STRIDE_F4 + TILE_HDR_F4) + TI_LEN + c);
                 const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[lane], clen));
                 // the same acceptance as a candidate of the tile stream: r <= thr2, then score <= thr
                 if (r <= __ldg(&h->thr2) && sc <= __ldg(&h->thr)) {
@@ -800,6 +798,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 // the candidate's tile: the ring stage recorded in its entry
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
+                const float *Tf = reinterpret_cast<const float *>(T);
                 float r;
                 bool keep = true;
                 if (PAPER && PAPER_D2) {
@@ -809,35 +808,36 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                     // exact tie -> the caller's direct orientation; a candidate of the other orientation
                     // (kept only by the screen's superset) drops out here
                     const float4 a10 = fm[fl], E = fe[fl], Ez = fez[fl];
-                    const float4 *cq = T + c;
-                    const float4 q0 = cq[0], q20 = cq[20 * TILE];
+                    const float4 q0 = T[TI_P0 + c], q20 = T[TI_P20 + c];
                     const float e00 = d2(E.x, E.z, Ez.x, q0), e2020 = d2(E.y, E.w, Ez.y, q20);
                     const float e020 = d2(E.x, E.z, Ez.x, q20), e200 = d2(E.y, E.w, Ez.y, q0);
                     const float mi = fmaxf(e020, e200), md = fmaxf(e00, e2020);
-                    const int oinf = (mi < md || (mi == md && cq[W_FLIP * TILE].w != 0.f)) ? 1 : 0;
+                    const int oinf = (mi < md || (mi == md && Tf[TI_FLIP + c] != 0.f)) ? 1 : 0;
                     keep = o == oinf;
-                    r = fmaxf(d2(a10.x, a10.y, a10.z, cq[10 * TILE]), o ? mi : md);
+                    r = fmaxf(d2(a10.x, a10.y, a10.z, T[TI_P10 + c]), o ? mi : md);
                 } else {
                     // exact mode screened with estimates: the 3-point running max, exactly as the
                     // dense test2 of the d2 form computes it (d2 and d2_pair_b agree bit for bit)
                     const float4 a10 = fm[fl], E = fe[fl], Ez = fez[fl];
-                    const float4 *cq = T + c;
-                    r = fmaxf(fmaxf(d2(a10.x, a10.y, a10.z, cq[10 * TILE]),
-                                    d2(E.x, E.z, Ez.x, cq[o ? 20 * TILE : 0])),
-                              d2(E.y, E.w, Ez.y, cq[o ? 0 : 20 * TILE]));
+                    r = fmaxf(fmaxf(d2(a10.x, a10.y, a10.z, T[TI_P10 + c]),
+                                    d2(E.x, E.z, Ez.x, T[(o ? TI_P20 : TI_P0) + c])),
+                              d2(E.y, E.w, Ez.y, T[(o ? TI_P0 : TI_P20) + c]));
                 }
                 const float thr2 = reinterpret_cast<const TileHdr *>(estage)->thr2;
                 const float thr = reinterpret_cast<const TileHdr *>(estage)->thr;
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
                 const float taul = MULTI ? (has_bundle(fl, b) ? -1.f : thr2) : fminf(thr2, key_cut2<PAPER>(best[fl]));
                 if (keep && r <= taul) {  // re-check against the freshest best (an earlier round of this tile may have lowered it)
-                    const float4 *cb = T + c + (o ? 20 * TILE : 0);
-                    const int st = o ? -TILE : TILE;
+                    // the centroid's middle points in the caller's order: slot k, or TILE_MID - 1 - k reversed
+                    const int cofs = c + (o ? (TILE_MID - 1) * TILE : 0), st = o ? -TILE : TILE;
+                    const float2 *cxy = reinterpret_cast<const float2 *>(Tf + TI_MXY) + cofs;
+                    const float *cz = Tf + TI_MZ + cofs;
                     bool done = false;
-#define SEG_STEP(i)                                                             \
-    {                                                                           \
-const float2 a = fxy[mid_slot(i) * PP + fl];                            \
-r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
+#define SEG_STEP(i)                                                                                  \
+    {                                                                                                \
+const float2 a = fxy[mid_slot(i) * PP + fl];                                                 \
+const float2 b = cxy[mid_slot(i) * st];                                                      \
+r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mid_slot(i) * st], 0.f))); \
     }
                     if (STATS) cnt[ST_T34]++;
                     SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
@@ -860,7 +860,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         // a7: lexicographic (d^2, bundle) minimum; paper mode: (d_ME + TN, bundle)
                         if (PAPER) {
                             if (r <= taul) {
-                                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], T[W_LEN * TILE + c].w));
+                                const float sc = __fadd_rn(__fsqrt_rn(r), tn_f32(flen[fl], Tf[TI_LEN + c]));
                                 if (sc <= thr) {
                                     const unsigned long long kk = ((unsigned long long)__float_as_uint(sc) << 32) | (uint32_t)b;
                                     atomicMin(best + fl, kk);
@@ -941,8 +941,8 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                     if ((pm >> lane) & 1u) { cnt[ST_LT_PASS]++; cnt[ST_T1] += TILE; cnt[ST_PDIST] += TILE; }
                 }
                 // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
-                const float4 c10 = T[10 * TILE + lane];
-                const float4 c0 = T[lane], c20 = T[20 * TILE + lane];
+                const float4 c10 = T[TI_P10 + lane];
+                const float4 c0 = T[TI_P0 + lane], c20 = T[TI_P20 + lane];
 #pragma unroll DENSE_UNROLL
                 while (pm) {
                     // FB fibers per step: independent chains (ILP) and one warp vote per step
@@ -993,10 +993,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], cb[(i) * st]));    \
                         if (PAPER && PAPER_D2) {
                             // the paper infers the direction from the end points:
                             // argmin of the end-point maxima, ties -> the caller's direct orientation
-                            // (reading R17; the W_FLIP slot marks a centroid stored reversed); only that
+                            // (reading R17; the TI_FLIP word marks a centroid stored reversed); only that
                             // orientation goes on
                             const float mi = fmaxf(R20.x, R0.y), md = fmaxf(R0.x, R20.y);
-                            if (mi < md || (mi == md && T[W_FLIP * TILE + lane].w != 0.f)) rdv[q] = INFINITY;
+                            if (mi < md || (mi == md && reinterpret_cast<const float *>(T)[TI_FLIP + lane] != 0.f)) rdv[q] = INFINITY;
                             else riv[q] = INFINITY;
                         }
                         tjv[q] = tj;
@@ -1261,9 +1261,9 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
                 const TileHdr *h = reinterpret_cast<const TileHdr *>(tile);
                 const float4 *T = tile + TILE_HDR_F4;
                 thr2 = __ldg(&h->thr2);
-                c10 = __ldg(T + 10 * TILE + lane);
-                c0 = __ldg(T + lane);
-                c20 = __ldg(T + 20 * TILE + lane);
+                c10 = __ldg(T + TI_P10 + lane);
+                c0 = __ldg(T + TI_P0 + lane);
+                c20 = __ldg(T + TI_P20 + lane);
             }
             const float4 Ej = make_float4(__shfl_sync(0xffffffffu, E.x, j), __shfl_sync(0xffffffffu, E.y, j),
                                           __shfl_sync(0xffffffffu, E.z, j), __shfl_sync(0xffffffffu, E.w, j));

@@ -415,14 +415,24 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
             for (int i = 0; i < NPTS; ++i) {
                 const int src = P.flipped[m] ? (NPTS - 1 - i) : i;
                 const float *c = &cents[(size_t)m * 3 * NPTS + 3 * src];
-                // w: points 0, 10, 20 carry the lowered half squared norm of k_classify's dot-product screen
-                // (seg_internal.cuh), both modes; paper mode also -- point 1 the chord length (Eq. 3), point 2
-                // a 1 when the centroid is stored reversed (an exact end-point tie then picks the caller's
-                // direct orientation, so the result does not depend on the stored order)
+                // points 0, 10, 20 carry the lowered half squared norm of k_classify's dot-product screen in w
+                // (seg_internal.cuh), both modes; paper mode also the chord length (Eq. 3) and a 1 when the
+                // centroid is stored reversed (an exact end-point tie then picks the caller's direct
+                // orientation, so the result does not depend on the stored order)
                 const bool paper = (flags & SEG_MODE_PAPER) != 0;
-                const float w = (i == 0 || i == 10 || i == 20) ? screen_half_norm_host(c)
-                                : !paper ? 0.f : i == 1 ? clen[(size_t)m] : i == 2 ? (P.flipped[m] ? 1.f : 0.f) : 0.f;
-                tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4 + (size_t)i * TILE + k] = make_float4(c[0], c[1], c[2], w);
+                float4 *t4 = &tiles[(size_t)t * TILE_STRIDE_F4 + TILE_HDR_F4];
+                float *tf = reinterpret_cast<float *>(t4);
+                if (i == 0 || i == 10 || i == 20) {
+                    t4[(i == 0 ? TI_P0 : i == 10 ? TI_P10 : TI_P20) + k] = make_float4(c[0], c[1], c[2], screen_half_norm_host(c));
+                } else {
+                    tf[TI_MXY + 2 * (mid_slot(i) * TILE + k)] = c[0];
+                    tf[TI_MXY + 2 * (mid_slot(i) * TILE + k) + 1] = c[1];
+                    tf[TI_MZ + mid_slot(i) * TILE + k] = c[2];
+                }
+                if (i == 0) {
+                    tf[TI_LEN + k] = paper ? clen[(size_t)m] : 0.f;
+                    tf[TI_FLIP + k] = paper && P.flipped[m] ? 1.f : 0.f;
+                }
                 tiles_cm[((size_t)t * TILE + k) * NPTS + i] = make_float4(c[0], c[1], c[2], 0.f);
                 for (int d = 0; d < 3; ++d) {
                     lo[d] = std::min(lo[d], c[d]);

@@ -18,10 +18,24 @@ namespace seg {
 
 constexpr int NPTS = 21;                 // points per fiber / centroid
 constexpr int TILE = 32;                 // centroids per tile (one bit per centroid in a u32 mask)
-constexpr int TILE_F4 = NPTS * TILE;     // float4 of tile point data: [21 points][32 centroids]
+constexpr int TILE_MID = NPTS - 3;       // points other than 0, 10, 20
+// plane slot of point i (i != 0, 10, 20) among the middle points; the reversed point 20 - i sits in slot
+// TILE_MID - 1 - mid_slot(i)
+__host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
+// The tile image (one 1-D TMA bulk copy) after its 112-B TileHdr: points 0 / 10 / 20 of the 32 centroids as
+// float4 (w = the screen's lowered half norm, Sec. below); per centroid the chord length and a stored-reversed
+// flag (paper mode, else 0); then the 18 middle points as an xy plane (float2) and a z plane, [slot][centroid]
+// -- no unused w words, so four stages fit in k_classify's shared memory
+constexpr int TI_P0 = 0, TI_P10 = TILE, TI_P20 = 2 * TILE;   // float4 index after the header
+constexpr int TI_LEN = 3 * TILE * 4;                          // float index: chord length [32]
+constexpr int TI_FLIP = TI_LEN + TILE;                        // float index: 1 = stored reversed [32]
+constexpr int TI_MXY = TI_FLIP + TILE;                        // float index: xy plane [18][32] of float2
+constexpr int TI_MZ = TI_MXY + 2 * TILE_MID * TILE;           // float index: z plane [18][32]
+constexpr int TILE_F4 = (TI_MZ + TILE_MID * TILE) / 4;        // 544 float4 of tile data
+static_assert((TI_MZ + TILE_MID * TILE) % 4 == 0 && TI_MXY % 2 == 0, "tile image layout");
 constexpr int TILE_HDR_F4 = 7;           // the tile's 112-B TileHdr travels in front of its data
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
-constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 10,864 B -> one 1-D TMA bulk copy
+constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 8,816 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
 
 // Exact mode's dot-product screen for test1 / test2.  Each squared distance of the

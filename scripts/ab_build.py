@@ -1,5 +1,5 @@
 """A/B timing of library builds with extra nvcc defines: python scripts/ab_build.py CFG "-DX" "-DY" ...
-(the empty string = production).  AB_MODE=paper: paper-semantics atlases.  Prints the per-kernel event times from seg_profile_read."""
+(the empty string = production; "lib:PATH" = a prebuilt library).  AB_MODE=paper: paper-semantics atlases.  Prints the per-kernel event times from seg_profile_read."""
 import ctypes, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -16,9 +16,12 @@ N = fib.shape[0]
 c, b, t = (torch.from_numpy(x).cuda() for x in (at.centroids, at.bundle_id, at.thresh))
 ref = None
 for k, d in enumerate(defs):
-    out = os.path.abspath(f"build/ab/lib{k}.so")
-    subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, *d.split(), "-o", out, *_build.SOURCES],
-                          stderr=subprocess.DEVNULL)
+    if d.startswith("lib:"):   # a prebuilt library (e.g. the previous commit's, built here before the call)
+        out = os.path.abspath(d[4:])
+    else:
+        out = os.path.abspath(f"build/ab/lib{k}.so")
+        subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, *d.split(), "-o", out, *_build.SOURCES],
+                              stderr=subprocess.DEVNULL)
     L = ctypes.CDLL(out)
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     L.seg_create.argtypes = [vp, vp, i64, vp, i32, ctypes.c_int, ctypes.POINTER(vp)]
