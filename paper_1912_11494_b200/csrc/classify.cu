@@ -426,6 +426,9 @@ constexpr int PP = SEG_PLANE_PITCH;
 #ifndef SEG_Q2CAP
 #define SEG_Q2CAP 128
 #endif
+constexpr int MULTI_WORDS = 4;         // multi-label masks: at most 128 bundles (they live in the q2r region)
+// the q2r region per warp: the stack's 3-point values (PAPER_D2 builds only) or the 32 fibers' masks (MULTI)
+constexpr int Q2R_WORDS = (PAPER_D2 && SEG_Q2CAP > 32 * MULTI_WORDS) ? SEG_Q2CAP : 32 * MULTI_WORDS;
 constexpr int Q2CAP = SEG_Q2CAP;       // candidate stack; flushed when fewer than 64 slots remain (128: room for the 4th ring stage)
 constexpr int PECAP = 32;              // MULTI: winners of one tile (at most one per fiber)
 constexpr uint32_t SLEEP_NS = 1000000; // mbarrier try_wait suspend-time hint
@@ -464,7 +467,7 @@ struct SmemLayout {
         best = o; o += (size_t)FPC * sizeof(unsigned long long);
         flen = o; o += (size_t)FPC * sizeof(float);          // paper mode: chord length of each fiber
         bars = o; o += 2 * STAGES * sizeof(uint64_t);
-        q2r = o;  o += (size_t)NCW * Q2CAP * sizeof(float);
+        q2r = o;  o += (size_t)NCW * Q2R_WORDS * sizeof(float);
         q2e = o;  o += (size_t)NCW * Q2CAP * sizeof(uint16_t);
         pe = o;   o += (size_t)NCW * PECAP * sizeof(uint16_t);
         meta = o; o += (size_t)STAGES * sizeof(StageMeta);
@@ -537,7 +540,6 @@ __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez,
 // MULTI (row f4's optional half, PAPER.md:163's original DWM assignment): every bundle within its threshold,
 // as a bit mask per fiber (exact mode only).  The cascade is the same with the cutoff thr_b (no best-so-far
 // across bundles), a bundle already accepted for a fiber is skipped, and an accepted candidate ORs its bit.
-constexpr int MULTI_WORDS = 4;          // at most 128 bundles; the masks live in the q2r region (paper-D2 only)
 template <bool STATS, bool PAPER, bool MULTI = false>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -568,9 +570,9 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     uint16_t *pe = reinterpret_cast<uint16_t *>(smem + L.pe) + cw * PECAP;     // MULTI: the tile's winners, same format
     // MULTI: this warp's 32 fibers' masks ([32][MULTI_WORDS] words in the otherwise unused q2r region)
     uint32_t *mmask = reinterpret_cast<uint32_t *>(smem + L.q2r) + cw * 32 * MULTI_WORDS;
-    static_assert(NCW * 32 * MULTI_WORDS * sizeof(uint32_t) <= NCW * Q2CAP * sizeof(float), "masks fit in q2r");
+    static_assert(32 * MULTI_WORDS <= Q2R_WORDS && (!PAPER_D2 || Q2CAP <= Q2R_WORDS), "q2r region");
     auto has_bundle = [&](int f, int b) -> bool { return (mmask[f * MULTI_WORDS + (b >> 5)] >> (b & 31)) & 1u; };
-    float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2CAP;
+    float *q2r = reinterpret_cast<float *>(smem + L.q2r) + cw * Q2R_WORDS;
 
     // the producer lane sets up the ring and issues the first STAGES tile copies (or the end marker) at once,
     // so they land while the consumers ingest their fibers; the loop below continues from kpre
