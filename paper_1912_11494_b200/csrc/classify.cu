@@ -404,12 +404,19 @@ constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 #endif
 // fibers per step of the dense test1+test2 loop (a warp-tile holds ~11 passing fibers).  Exact mode, with
 // the dot-product screen: 1 since round 2's bank-conflict and branch fixes (cfg 3 -1.1%, cfg 4 -1.6% vs 2;
-// 3: +1.5%); round 1 had measured 2 best.  Paper mode, d2 form, with the per-fiber VOTE: 2 (1: +0.9%).
+// 3: +1.5%); round 1 had measured 2 best.  Paper mode: 2 until the next fiber was picked one step ahead
+// (SEG_JNEXT), which only the one-fiber step can do: then 1 (cfg 3 4.80 -> 4.65 ms, cfg 4 -3.6%).
 #ifndef SEG_FB
 #define SEG_FB 1
 #endif
+#ifndef SEG_RPRE
+#define SEG_RPRE 0   // candidate rounds: test3's points loaded with the three-point ones
+#endif
+#ifndef SEG_JNEXT
+#define SEG_JNEXT 1   // FB == 1: the next dense step's fiber picked during the current step
+#endif
 #ifndef SEG_FB_PAPER
-#define SEG_FB_PAPER 2
+#define SEG_FB_PAPER 1
 #endif
 constexpr int NMID = NPTS - 3;         // fiber points other than 0, 10, 20 (smem planes)
 // pitch of one point's plane (32 fibers) in the per-warp fxy (float2) and fz (float) arrays.  33, not 32: the
@@ -519,10 +526,41 @@ __device__ __forceinline__ float box_d2(float x, float y, float z, const float4 
 }
 // a2 with boxes: for every centroid c of the tile, |f_p - c_p| >= dist(f_p, box_p) (c_p lies in box_p);
 // the same orientation logic as the spheres.  Skip iff the bound exceeds s = sqrt(tau) + CULL_EPS.
+#if SEG_PAIRBOX
+__device__ __forceinline__ u64 sub_pair(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// per half: max(lo - x, x - hi, 0), the same values as box_d2's scalar gaps
+__device__ __forceinline__ u64 box_gap_pair(u64 x, float lo_a, float lo_b, float hi_a, float hi_b) {
+    const float2 a = upk2(sub_pair(pk2(lo_a, lo_b), x)), b = upk2(sub_pair(x, pk2(hi_a, hi_b)));
+    return pk2(fmaxf(fmaxf(a.x, b.x), 0.f), fmaxf(fmaxf(a.y, b.y), 0.f));
+}
+__device__ __forceinline__ float2 sq3_pair(u64 gx, u64 gy, u64 gz) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(gx));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(gy), "l"(r));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(gz), "l"(r));
+    return upk2(r);
+}
+#endif
 __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez, const float4 &F10,
                                               const TileHdr &h, float s) {
     const float s2 = s * s;
-#ifdef SEG_BOX_SHORTCIRCUIT
+#if SEG_PAIRBOX
+    // the four end-point box distances as two packed pairs (direct: (0 vs box 0, 20 vs box 20); inverse:
+    // (0 vs box 20, 20 vs box 0)), bit for bit box_d2's values; combined without short-circuits as below
+    const bool p10 = box_d2(F10.x, F10.y, F10.z, h.lo10, h.hi10) <= s2;
+    const u64 X = pk2(E.x, E.y), Y = pk2(E.z, E.w), Z = pk2(Ez.x, Ez.y);
+    const float2 dd = sq3_pair(box_gap_pair(X, h.dxy_lo.x, h.dxy_lo.y, h.dxy_hi.x, h.dxy_hi.y),
+                               box_gap_pair(Y, h.dxy_lo.z, h.dxy_lo.w, h.dxy_hi.z, h.dxy_hi.w),
+                               box_gap_pair(Z, h.dz.x, h.dz.y, h.dz.z, h.dz.w));
+    const float2 di = sq3_pair(box_gap_pair(X, h.ixy_lo.x, h.ixy_lo.y, h.ixy_hi.x, h.ixy_hi.y),
+                               box_gap_pair(Y, h.ixy_lo.z, h.ixy_lo.w, h.ixy_hi.z, h.ixy_hi.w),
+                               box_gap_pair(Z, h.iz.x, h.iz.y, h.iz.z, h.iz.w));
+    return p10 & (((dd.x <= s2) & (dd.y <= s2)) | ((di.x <= s2) & (di.y <= s2)));
+#elif defined(SEG_BOX_SHORTCIRCUIT)
     const bool p10 = box_d2(F10.x, F10.y, F10.z, h.lo10, h.hi10) <= s2;
     const bool pdir = box_d2(E.x, E.z, Ez.x, h.lo0, h.hi0) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo20, h.hi20) <= s2;
     const bool pinv = box_d2(E.x, E.z, Ez.x, h.lo20, h.hi20) <= s2 && box_d2(E.y, E.w, Ez.y, h.lo0, h.hi0) <= s2;
@@ -801,6 +839,24 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const float4 *estage = ring + es * TILE_STRIDE_F4;
                 const float4 *T = estage + TILE_HDR_F4;
                 const float *Tf = reinterpret_cast<const float *>(T);
+                // the centroid's middle points in the caller's order: slot k, or TILE_MID - 1 - k reversed
+                const int cofs = c + (o ? (TILE_MID - 1) * TILE : 0), st = o ? -TILE : TILE;
+                const float2 *cxy = reinterpret_cast<const float2 *>(Tf + TI_MXY) + cofs;
+                const float *cz = Tf + TI_MZ + cofs;
+#if SEG_RPRE
+                // test3's four points loaded with the three-point ones (one shared-memory latency less on the
+                // round's chain)
+                constexpr int G1[4] = {3, 17, 7, 13};
+                float2 g1a[4], g1b[4];
+                float g1az[4], g1bz[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    g1a[k] = fxy[mid_slot(G1[k]) * PP + fl];
+                    g1az[k] = fz[mid_slot(G1[k]) * PP + fl];
+                    g1b[k] = cxy[mid_slot(G1[k]) * st];
+                    g1bz[k] = cz[mid_slot(G1[k]) * st];
+                }
+#endif
                 float r;
                 bool keep = true;
                 if (PAPER && PAPER_D2) {
@@ -830,10 +886,6 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const int b = reinterpret_cast<const TileHdr *>(estage)->bundle;
                 const float taul = MULTI ? (has_bundle(fl, b) ? -1.f : thr2) : fminf(thr2, key_cut2<PAPER>(best[fl]));
                 if (keep && r <= taul) {  // re-check against the freshest best (an earlier round of this tile may have lowered it)
-                    // the centroid's middle points in the caller's order: slot k, or TILE_MID - 1 - k reversed
-                    const int cofs = c + (o ? (TILE_MID - 1) * TILE : 0), st = o ? -TILE : TILE;
-                    const float2 *cxy = reinterpret_cast<const float2 *>(Tf + TI_MXY) + cofs;
-                    const float *cz = Tf + TI_MZ + cofs;
                     bool done = false;
 #define SEG_STEP(i)                                                                                  \
     {                                                                                                \
@@ -842,7 +894,13 @@ const float2 b = cxy[mid_slot(i) * st];                                         
 r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mid_slot(i) * st], 0.f))); \
     }
                     if (STATS) cnt[ST_T34]++;
+#if SEG_RPRE
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        r = fmaxf(r, d2(g1a[k].x, g1a[k].y, g1az[k], make_float4(g1b[k].x, g1b[k].y, g1bz[k], 0.f)));
+#else
                     SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
+#endif
                     if (STATS) cnt[ST_PDIST] += 4;
                     if (r > taul) done = true;
                     if (!done) {
@@ -945,13 +1003,30 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
                 // ---- a3 + a4, dense and transposed: lane = centroid, the warp walks its fibers ----
                 const float4 c10 = T[TI_P10 + lane];
                 const float4 c0 = T[TI_P0 + lane], c20 = T[TI_P20 + lane];
+                constexpr int FB = PAPER ? SEG_FB_PAPER : SEG_FB;
+#if SEG_JNEXT
+                // one fiber per step (FB == 1): the next step's fiber is found during this step (highest set bit
+                // first, FLO), so its FLO -> LEA -> LDS latency stays off the step's dependent chain (cfg 3 -3%,
+                // paper -2.5%; the same for every fiber of an FB = 2 step, or the cutoff shuffle moved along too:
+                // both lose)
+                int jnext;
+                asm("bfind.u32 %0, %1;" : "=r"(jnext) : "r"(pm));
+#endif
 #pragma unroll DENSE_UNROLL
                 while (pm) {
                     // FB fibers per step: independent chains (ILP) and one warp vote per step
-                    constexpr int FB = PAPER ? SEG_FB_PAPER : SEG_FB;
                     int jj[FB];
                     float rdv[FB], riv[FB], tjv[FB];
                     uint32_t hit = 0;
+#if SEG_JNEXT
+                    if (FB == 1) {
+                        uint32_t below;
+                        jj[0] = jnext;
+                        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(jnext));   // the bits below jnext
+                        pm &= below;
+                        asm("bfind.u32 %0, %1;" : "=r"(jnext) : "r"(pm));             // -1 once pm is empty
+                    } else
+#endif
 #pragma unroll
                     for (int q = 0; q < FB; ++q) {
                         // highest set bit first: FLO gives the index directly, and -1 once pm is empty

@@ -462,12 +462,22 @@ extern "C" int seg_create_ex(const float *centroids, const int32_t *bundle_id, i
                     }
                 }
             }
-            th[t].lo0 = make_float4(blo[0][0], blo[0][1], blo[0][2], 0.f);
-            th[t].hi0 = make_float4(bhi[0][0], bhi[0][1], bhi[0][2], 0.f);
             th[t].lo10 = make_float4(blo[1][0], blo[1][1], blo[1][2], 0.f);
             th[t].hi10 = make_float4(bhi[1][0], bhi[1][1], bhi[1][2], 0.f);
+#if SEG_PAIRBOX
+            // end-point boxes as (point 0, point 20) pairs and swapped (seg_internal.cuh)
+            th[t].dxy_lo = make_float4(blo[0][0], blo[2][0], blo[0][1], blo[2][1]);
+            th[t].dxy_hi = make_float4(bhi[0][0], bhi[2][0], bhi[0][1], bhi[2][1]);
+            th[t].dz = make_float4(blo[0][2], blo[2][2], bhi[0][2], bhi[2][2]);
+            th[t].ixy_lo = make_float4(blo[2][0], blo[0][0], blo[2][1], blo[0][1]);
+            th[t].ixy_hi = make_float4(bhi[2][0], bhi[0][0], bhi[2][1], bhi[0][1]);
+            th[t].iz = make_float4(blo[2][2], blo[0][2], bhi[2][2], bhi[0][2]);
+#else
+            th[t].lo0 = make_float4(blo[0][0], blo[0][1], blo[0][2], 0.f);
+            th[t].hi0 = make_float4(bhi[0][0], bhi[0][1], bhi[0][2], 0.f);
             th[t].lo20 = make_float4(blo[2][0], blo[2][1], blo[2][2], 0.f);
             th[t].hi20 = make_float4(bhi[2][0], bhi[2][1], bhi[2][2], 0.f);
+#endif
         }
         {
             const double sv = (double)thr[b] + (double)CULL_EPS;

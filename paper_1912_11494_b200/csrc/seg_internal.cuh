@@ -33,9 +33,13 @@ constexpr int TI_MXY = TI_FLIP + TILE;                        // float index: xy
 constexpr int TI_MZ = TI_MXY + 2 * TILE_MID * TILE;           // float index: z plane [18][32]
 constexpr int TILE_F4 = (TI_MZ + TILE_MID * TILE) / 4;        // 544 float4 of tile data
 static_assert((TI_MZ + TILE_MID * TILE) % 4 == 0 && TI_MXY % 2 == 0, "tile image layout");
-constexpr int TILE_HDR_F4 = 7;           // the tile's 112-B TileHdr travels in front of its data
+// -DSEG_PAIRBOX=0: the round-2 header (112 B, the six end-point boxes as float4 lo / hi per point)
+#ifndef SEG_PAIRBOX
+#define SEG_PAIRBOX 1
+#endif
+constexpr int TILE_HDR_F4 = SEG_PAIRBOX ? 9 : 7;   // the tile's TileHdr (144 B) travels in front of its data
 constexpr int TILE_STRIDE_F4 = TILE_HDR_F4 + TILE_F4;
-constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 8,816 B -> one 1-D TMA bulk copy
+constexpr int TILE_STRIDE_BYTES = TILE_STRIDE_F4 * 16;  // 8,848 B -> one 1-D TMA bulk copy
 constexpr float CULL_EPS = 1e-3f;        // mm margin on every sphere lower bound
 
 // Exact mode's dot-product screen for test1 / test2.  Each squared distance of the
@@ -70,12 +74,26 @@ __host__ __device__ constexpr int morton_bits_for(int n) { return n >= MORTON_FI
 // centroid points 0, 10, 20 over the tile's members (exact FP32 min / max, canonical orientation): the
 // live tile bound of k_classify.  Boxes leave 0.59-0.81 of the spheres' (fiber, tile) passes at the live
 // cutoff; k_cull keeps spheres (CullTile) for its threshold-only list.
+// The end-point boxes are stored as f32x2 pairs matching the fiber's packed end points (x0, x20), (y0, y20),
+// (z0, z20), so the four end-point box distances take packed FADD2 / FMUL2 / FFMA2 (bit for bit the scalar
+// values): d* = (box of point 0, box of point 20) for the direct orientation, i* = (box 20, box 0) for the
+// inverse one.
 struct __align__(16) TileHdr {
     int bundle;
     float thr2;
     float thr;
     int pad;
+#if SEG_PAIRBOX
+    float4 lo10, hi10;
+    float4 dxy_lo;   // (lo0.x, lo20.x, lo0.y, lo20.y)
+    float4 dxy_hi;   // (hi0.x, hi20.x, hi0.y, hi20.y)
+    float4 dz;       // (lo0.z, lo20.z, hi0.z, hi20.z)
+    float4 ixy_lo;   // (lo20.x, lo0.x, lo20.y, lo0.y)
+    float4 ixy_hi;   // (hi20.x, hi0.x, hi20.y, hi0.y)
+    float4 iz;       // (lo20.z, lo0.z, hi20.z, hi0.z)
+#else
     float4 lo0, hi0, lo10, hi10, lo20, hi20;
+#endif
 };
 static_assert(sizeof(TileHdr) == 16 * TILE_HDR_F4, "TileHdr fills TILE_HDR_F4 float4");
 

@@ -1,4 +1,7 @@
-"""Summarise an ncu report: key SOL/scheduler metrics, stall reasons and per-source-line hot spots."""
+"""Summarise an ncu report: key SOL/scheduler metrics, stall reasons and per-source-line hot spots.
+
+    python scripts/ncu_summary.py REPORT.ncu-rep [TOP_LINES] [KERNEL_REGEX]
+"""
 import csv
 import io
 import subprocess
@@ -6,10 +9,12 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+kern = sys.argv[3] if len(sys.argv) > 3 else None   # a kernel-name regex, for reports holding several kernels
 
 
 def ncu(*args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    filt = ["-k", f"regex:{kern}"] if kern else []
+    return subprocess.run(["ncu", "-i", rep, *filt, *args], capture_output=True, text=True).stdout
 
 
 rows = list(csv.reader(io.StringIO(ncu("--page", "details", "--csv"))))
