@@ -409,9 +409,6 @@ constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 #ifndef SEG_FB
 #define SEG_FB 1
 #endif
-#ifndef SEG_RPRE
-#define SEG_RPRE 0   // candidate rounds: test3's points loaded with the three-point ones
-#endif
 #ifndef SEG_JNEXT
 #define SEG_JNEXT 1   // FB == 1: the next dense step's fiber picked during the current step
 #endif
@@ -843,20 +840,6 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 const int cofs = c + (o ? (TILE_MID - 1) * TILE : 0), st = o ? -TILE : TILE;
                 const float2 *cxy = reinterpret_cast<const float2 *>(Tf + TI_MXY) + cofs;
                 const float *cz = Tf + TI_MZ + cofs;
-#if SEG_RPRE
-                // test3's four points loaded with the three-point ones (one shared-memory latency less on the
-                // round's chain)
-                constexpr int G1[4] = {3, 17, 7, 13};
-                float2 g1a[4], g1b[4];
-                float g1az[4], g1bz[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    g1a[k] = fxy[mid_slot(G1[k]) * PP + fl];
-                    g1az[k] = fz[mid_slot(G1[k]) * PP + fl];
-                    g1b[k] = cxy[mid_slot(G1[k]) * st];
-                    g1bz[k] = cz[mid_slot(G1[k]) * st];
-                }
-#endif
                 float r;
                 bool keep = true;
                 if (PAPER && PAPER_D2) {
@@ -894,13 +877,7 @@ const float2 b = cxy[mid_slot(i) * st];                                         
 r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mid_slot(i) * st], 0.f))); \
     }
                     if (STATS) cnt[ST_T34]++;
-#if SEG_RPRE
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        r = fmaxf(r, d2(g1a[k].x, g1a[k].y, g1az[k], make_float4(g1b[k].x, g1b[k].y, g1bz[k], 0.f)));
-#else
                     SEG_STEP(3); SEG_STEP(17); SEG_STEP(7); SEG_STEP(13);
-#endif
                     if (STATS) cnt[ST_PDIST] += 4;
                     if (r > taul) done = true;
                     if (!done) {
