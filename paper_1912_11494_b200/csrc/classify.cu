@@ -955,6 +955,10 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
                                     : fminf(thr2, key_cut2<PAPER>(best[lane]));
             constexpr bool D2FORM = SCREEN_OFF || (PAPER && PAPER_D2);
             const float tcmp = D2FORM ? tau : __fmul_rn(tau, 0.5f);   // the screen works at half scale
+            // paper mode: this lane's stack-entry bits for the tile, opaque to the compiler (it would re-derive
+            // the lane index with an S2R on every hit): paper -1.5%; exact mode +0.2%, so it keeps the plain form
+            uint32_t ebase = 0;
+            if (PAPER) asm volatile("mov.b32 %0, %1;" : "=r"(ebase) : "r"((uint32_t)(lane | (s << 11))));
             // a2 with the live cutoff: the exact sphere bound of this lane's fiber vs the tile
             // MUFU.SQRT (relative error < 2^-22) raised by 2^-20 so the radius never falls below the
             // exact one: no IEEE slow-path branch on the per-tile chain
@@ -1082,7 +1086,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
                         // best 3-point survivor to a winners' round first, for its fresher cutoff: one more round
                         // per tile, which costs more than its pruning saves -- DESIGN.md Sec. 5)
                         if (STATS && lane == 0) cnt[ST_HITS]++;
-                        const uint32_t e = (uint32_t)((j << 5) | lane | (s << 11));
+                        const uint32_t e = PAPER ? ebase | (uint32_t)(j << 5) : (uint32_t)((j << 5) | lane | (s << 11));
                         bool qd = ad, qi = ai;
                         if (MULTI) {
                             // multi-label masks keep a winners' round: one accepted centroid settles the bundle
