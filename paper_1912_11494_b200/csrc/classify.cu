@@ -22,8 +22,6 @@
 #include <climits>
 #include <cstdint>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include "seg_internal.cuh"
 
 namespace seg {
@@ -268,49 +266,7 @@ __global__ void k_morton_scatter(MortonParams p) {
     p.perm[pos] = i;
 }
 
-// The prepass as a radix sort instead: k_morton_key writes every fiber's key and its index, and CUB's
-// onesweep radix sort (stable, 3 x bits key bits) orders the indices.  The histogram form above serialises its
-// atomics on the crowded cells (matched fibers cluster around the bundles' midpoints: k_morton_hist 179 us
-// at cfg 3); the sort has no hot spots.  Stable, so the order inside a cell is the input order.
-__global__ void k_morton_key(MortonParams p) {
-    const float lim = (float)((1 << p.bits) - 1);
-    const float sc = (float)(1 << (p.bits - MORTON_BITS));
-    const int i0 = blockIdx.x * blockDim.x * MORTON_FPT + threadIdx.x;
-    float v[MORTON_FPT][3];
-#pragma unroll
-    for (int q = 0; q < MORTON_FPT; ++q) {
-        const int i = i0 + q * blockDim.x;
-        const float *f = p.fibers + (size_t)min(i, p.n - 1) * (3 * NPTS) + 30;  // point 10
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v[q][c] = __ldg(f + c);
-    }
-#pragma unroll
-    for (int q = 0; q < MORTON_FPT; ++q) {
-        const int i = i0 + q * blockDim.x;
-        if (i >= p.n) break;
-        const float qx = fminf(fmaxf((v[q][0] - p.lo.x) * (p.inv_cell.x * sc), 0.f), lim);
-        const float qy = fminf(fmaxf((v[q][1] - p.lo.y) * (p.inv_cell.y * sc), 0.f), lim);
-        const float qz = fminf(fmaxf((v[q][2] - p.lo.z) * (p.inv_cell.z * sc), 0.f), lim);
-        p.key[i] = spread3((uint32_t)qx) | (spread3((uint32_t)qy) << 1) | (spread3((uint32_t)qz) << 2);
-        p.rank[i] = (uint32_t)i;   // the value the sort carries
-    }
-}
-
-size_t morton_sort_temp_bytes(int n, int bits) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const int32_t *)nullptr, (int32_t *)nullptr, n, 0, 3 * bits);
-    return bytes;
-}
-
-cudaError_t launch_morton_sort(const MortonParams &p, uint32_t *keys_out, void *temp, size_t temp_bytes,
-                               cudaStream_t s) {
-    k_morton_key<<<(p.n + 256 * MORTON_FPT - 1) / (256 * MORTON_FPT), 256, 0, s>>>(p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, p.key, keys_out, reinterpret_cast<const int32_t *>(p.rank),
-                                           p.perm, p.n, 0, 3 * p.bits, s);
-}
+// (The prepass as CUB's onesweep radix sort of (key, index) was measured and rejected: DESIGN.md Sec. 5.)
 
 cudaError_t launch_morton_prepass(const MortonParams &p, cudaStream_t s) {
     const size_t buckets = (size_t)1 << (3 * p.bits);
@@ -409,6 +365,12 @@ constexpr int DENSE_UNROLL = SEG_DENSE_UNROLL;   // k_classify's dense step loop
 #ifndef SEG_FB
 #define SEG_FB 1
 #endif
+#ifndef SEG_NLIST
+#define SEG_NLIST 0     // consumers loop over the list length instead of reading an end marker per tile
+#endif
+#ifndef SEG_WAIT_NS
+#define SEG_WAIT_NS 0   // consumers' tile wait: try_wait + nanosleep(N) instead of the suspend-hinted try_wait
+#endif
 #ifndef SEG_JNEXT
 #define SEG_JNEXT 1   // FB == 1: the next dense step's fiber picked during the current step
 #endif
@@ -493,6 +455,15 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t *bar, uint32_t parity) 
         "@!P1 bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(SLEEP_NS)
         : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
 }
 
 __device__ __forceinline__ float key_d2(unsigned long long k) { return __uint_as_float((uint32_t)(k >> 32)); }
@@ -613,6 +584,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
     // so they land while the consumers ingest their fibers; the loop below continues from kpre
     const unsigned short *lst_g = reinterpret_cast<const unsigned short *>(p.tile_bits) + (size_t)cta * cull_stride(p.T);
     int kpre = 0, nlist = 0;
+    __shared__ int s_nlist;   // SEG_NLIST: the list length, for the consumers' loop bound
     if (threadIdx.x == FPC) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, 1);
@@ -622,7 +594,8 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         nlist = __ldg(lst_g);
         SEG_DCHECK(nlist >= 0 && nlist <= p.T);
 #if SEG_EARLY_TMA
-        for (; kpre < STAGES && kpre <= nlist; ++kpre) {
+        if (SEG_NLIST) s_nlist = nlist;   // visible to the consumers after the CTA barrier that ends the ingest
+        for (; kpre < STAGES && kpre < nlist + (SEG_NLIST ? 0 : 1); ++kpre) {
             if (kpre < nlist) {
                 const int t = __ldg(lst_g + 1 + kpre);
                 SEG_DCHECK(t >= 0 && t < p.T);
@@ -807,7 +780,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
                 mbar_arrive_expect_tx(full + s, TILE_STRIDE_BYTES);
                 bulk_g2s(ring + s * TILE_STRIDE_F4, p.tiles + (size_t)t * TILE_STRIDE_F4, TILE_STRIDE_BYTES, full + s);
             }
-            if (kpre <= nlist) {   // end of stream, unless it went out with the first copies
+            if (!SEG_NLIST && kpre <= nlist) {   // end of stream, unless it went out with the first copies
                 const int s = k % STAGES, u = k / STAGES;
                 if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
                 meta[s].tile = -1;
@@ -937,13 +910,18 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
         };
         long long tc0 = 0;
         if (STATS) tc0 = clock64();
-        for (int k = 0;; ++k) {
+        const int klim = SEG_NLIST ? s_nlist : 0x7fffffff;
+        for (int k = 0; k < klim; ++k) {
             const int s = k % STAGES, u = k / STAGES;
             long long tw0 = 0;
             if (STATS) tw0 = clock64();
+#if SEG_WAIT_NS
+            while (!mbar_try(full + s, u & 1)) __nanosleep(SEG_WAIT_NS);
+#else
             mbar_sleep_wait(full + s, u & 1);
+#endif
             if (STATS && lane == 0) cnt[ST_CYC_FULLWAIT] += clock64() - tw0;
-            if (meta[s].tile < 0) break;
+            if (!SEG_NLIST && meta[s].tile < 0) break;
             const float4 *stage = ring + s * TILE_STRIDE_F4;
             const TileHdr th = *reinterpret_cast<const TileHdr *>(stage);
             const float thr2 = th.thr2;
