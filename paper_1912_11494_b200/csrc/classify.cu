@@ -1171,12 +1171,22 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
 #ifndef SEG_CULL_XPOSE
 #define SEG_CULL_XPOSE 1   // k_cull's per-chunk pass / inside counts by a warp bit-matrix transpose (-4%)
 #endif
+#ifndef SEG_CULL_APPEND
+#define SEG_CULL_APPEND 1  // k_cull: tiles appended to the list as they are first marked (no list-building pass; -1.4%)
+#endif
+#ifndef SEG_CULL_WBOX
+#define SEG_CULL_WBOX 1   // k_cull: each warp's candidate bundles from the box of its points 10 (no CTA union; -8%)
+#endif
 #ifndef SEG_CULL_MAXREG_CTAS
 #define SEG_CULL_MAXREG_CTAS 5
 #endif
+// k_cull's dynamic shared memory: [twords + bwords + T] u32 (tile bits, bundle bits, priorities), [T] u16 list
+__host__ __device__ inline size_t cull_smem_bytes(int T, int B) {
+    return sizeof(uint32_t) * (size_t)(((T + 31) >> 5) + ((B + 31) >> 5) + T) + sizeof(uint16_t) * (size_t)T;
+}
 __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyParams p) {
     // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list (u16)
-    extern __shared__ uint32_t sbits[];
+    extern __shared__ __align__(16) uint32_t sbits[];
     const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
     uint32_t *tb = sbits, *bb = sbits + twords, *prio = bb + bwords;
     uint16_t *lst = reinterpret_cast<uint16_t *>(prio + p.T);
@@ -1185,6 +1195,7 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
     // the padding up to a multiple of 32) gets a centre at 1e30 so that no fiber passes it
     __shared__ float4 sbs[MAX_SMEM_BUNDLES];
     for (int i = threadIdx.x; i < twords + bwords + p.T; i += FPC) sbits[i] = 0;
+    if (SEG_CULL_APPEND && threadIdx.x == 0) nlist = 0;
     const bool stage_bh = p.B <= MAX_SMEM_BUNDLES;
     auto bsphere = [&](int b) {
         if (b >= p.B) return make_float4(1e30f, 1e30f, 1e30f, 0.f);
@@ -1213,6 +1224,34 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
     float nd2 = INFINITY;   // each fiber's nearest tile by its sphere centres: the seed's tile
     int ntile = -1;
     __syncthreads();
+#if SEG_CULL_WBOX
+    // each warp's candidate bundles, lane = bundle: the distance from the box of the warp's points 10 to a bundle's
+    // grown point-10 sphere, with d2's operation sequence, is never above a member fiber's own d2 (every rounding
+    // is monotone), so the candidates hold every bundle a fiber of the warp passes; each is re-tested per fiber
+    float blo[3], bhi[3];
+    {
+        const bool v = !isnan(F10.x);   // a non-finite fiber carries F10.x = NaN and passes nothing
+        blo[0] = v ? F10.x : INFINITY; blo[1] = v ? F10.y : INFINITY; blo[2] = v ? F10.z : INFINITY;
+        bhi[0] = v ? F10.x : -INFINITY; bhi[1] = v ? F10.y : -INFINITY; bhi[2] = v ? F10.z : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                blo[k] = fminf(blo[k], __shfl_xor_sync(0xffffffffu, blo[k], o));
+                bhi[k] = fmaxf(bhi[k], __shfl_xor_sync(0xffffffffu, bhi[k], o));
+            }
+    }
+    for (int w = 0; w < bwords; ++w) {
+        uint32_t bits;
+        {
+            const float4 c = stage_bh ? sbs[(w << 5) + lane] : bsphere((w << 5) + lane);   // padded past B
+            const float gx = fmaxf(fmaxf(__fsub_rn(blo[0], c.x), __fsub_rn(c.x, bhi[0])), 0.f);
+            const float gy = fmaxf(fmaxf(__fsub_rn(blo[1], c.y), __fsub_rn(c.y, bhi[1])), 0.f);
+            const float gz = fmaxf(fmaxf(__fsub_rn(blo[2], c.z), __fsub_rn(c.z, bhi[2])), 0.f);
+            bits = __ballot_sync(0xffffffffu, __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx))) <= c.w);
+        }
+        while (bits) {
+#else
     // bundles some fiber of the CTA may need (point-10 sphere + threshold, exact)
     for (int b0 = 0; b0 < p.B; b0 += 32) {
         uint32_t m = 0;
@@ -1228,6 +1267,7 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
     for (int w = 0; w < bwords; ++w) {
         uint32_t bits = bb[w];
         while (bits) {
+#endif
             const int b = (w << 5) + __ffs(bits) - 1;
             bits &= bits - 1;
             const float4 c = stage_bh ? sbs[b] : bsphere(b);
@@ -1295,7 +1335,13 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
 #endif
                 if (npass) {
                     const int t = t0 + lane;
+#if SEG_CULL_APPEND
+                    // the first lane to mark a tile appends it to the (unordered) list; the ranking below orders it
+                    const uint32_t bit = 1u << (t & 31);
+                    if (!(atomicOr(tb + (t >> 5), bit) & bit)) lst[atomicAdd(&nlist, 1)] = (uint16_t)t;
+#else
                     atomicOr(tb + (t >> 5), 1u << (t & 31));
+#endif
                     atomicAdd(prio + t, (uint32_t)nclose * 256u + (uint32_t)npass);
                 }
             }
@@ -1353,6 +1399,7 @@ __global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyPara
 seed_done:
 #endif
     __syncthreads();
+#if !SEG_CULL_APPEND
     // the CTA's tiles from the bit set (warp 0: prefix over the words), in tile order
     if (threadIdx.x < 32) {
         int base = 0;
@@ -1377,6 +1424,8 @@ seed_done:
         if (lane == 0) nlist = base;
     }
     __syncthreads();
+#endif
+    SEG_DCHECK(nlist <= p.T);
     // best-first order for k_classify: tiles that contain more of the CTA's fibers (inside all
     // three spheres) first, then tiles that more fibers may need, then the tile index.  Any order
     // gives the same result (the (d^2, bundle) minimum is order-independent); a good order makes
@@ -1501,9 +1550,7 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
     if (p.n <= 0) return cudaSuccess;
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
-    const size_t cull_smem = sizeof(uint32_t) * (size_t)(((p.T + 31) >> 5) + ((p.B + 31) >> 5) + p.T) +
-                             sizeof(uint16_t) * (size_t)p.T
-;
+    const size_t cull_smem = cull_smem_bytes(p.T, p.B);
     cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
     if (e != cudaSuccess) return e;
     k_cull<<<grid, FPC, cull_smem, s>>>(p);
