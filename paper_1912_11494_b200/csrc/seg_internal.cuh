@@ -22,7 +22,7 @@ constexpr int TILE_MID = NPTS - 3;       // points other than 0, 10, 20
 // plane slot of point i (i != 0, 10, 20) among the middle points; the reversed point 20 - i sits in slot
 // TILE_MID - 1 - mid_slot(i)
 __host__ __device__ constexpr int mid_slot(int i) { return i < 10 ? i - 1 : i - 2; }
-// The tile image (one 1-D TMA bulk copy) after its 112-B TileHdr: points 0 / 10 / 20 of the 32 centroids as
+// The tile image (one 1-D TMA bulk copy) after its 144-B TileHdr: points 0 / 10 / 20 of the 32 centroids as
 // float4 (w = the screen's lowered half norm, Sec. below); per centroid the chord length and a stored-reversed
 // flag (paper mode, else 0); then the 18 middle points as an xy plane (float2) and a z plane, [slot][centroid]
 // -- no unused w words, so four stages fit in k_classify's shared memory
