@@ -335,11 +335,9 @@ def main():
     value = pairs / (ms_step * 1e-3)
     fibers_per_s = n_job / (ms_step * 1e-3)
     clocks = clk.summary()
-    # hist, scan_blocks, scan_totals, scatter (N >= 4096), cull, cta_order (grids of <= 64 waves), classify; a grid
-    # of at most one wave (2 CTAs per SM) runs the cull inside k_classify (no k_cull / k_cta_order launch)
+    # hist, scan_blocks, scan_totals, scatter (N >= 4096), cull, cta_order (grids of <= 64 waves), classify
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    grid = -(-N // 256)
-    launches_per_step = (4 if N >= 4096 else 0) + (1 if grid <= 2 * sms else 2 + (1 if grid <= 64 * 2 * sms else 0))
+    launches_per_step = (4 if N >= 4096 else 0) + 2 + (1 if -(-N // 256) <= 64 * 2 * sms else 0)
     res_lab = out[0].cpu().numpy() if isinstance(out, tuple) else lab.cpu().numpy()
 
     # ---------------- stage counters + roofline of the dominant kernel ----------------

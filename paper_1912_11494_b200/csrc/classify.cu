@@ -551,15 +551,6 @@ __device__ __forceinline__ bool tile_may_pass(const float4 &E, const float2 &Ez,
 // MULTI (row f4's optional half, PAPER.md:163's original DWM assignment): every bundle within its threshold,
 // as a bit mask per fiber (exact mode only).  The cascade is the same with the cutoff thr_b (no best-so-far
 // across bundles), a bundle already accepted for a fiber is skipped, and an accepted candidate ORs its bit.
-__host__ __device__ inline size_t cull_smem_bytes(int T, int B);
-__device__ __forceinline__ void cull_window(const ClassifyParams &p, const int win, const int tid, const int nthr,
-                                            bool ok, const int myfidx, float4 E, float2 Ez, float4 F10,
-                                            uint32_t *sbits, float4 *sbs, int &nlist);
-#ifndef SEG_FUSE
-#define SEG_FUSE 1   // grids of at most one wave: k_classify culls its own window (k_cull's body, in the ring's space)
-#endif
-static_assert(!SEG_FUSE || SEG_NLIST, "the fused cull needs the list-length loop bound");
-
 template <bool STATS, bool PAPER, bool MULTI = false>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -605,8 +596,6 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
             mbar_init(empty + s, NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (threadIdx.x == FPC && !p.fused) {   // fused: the list exists only after the CTA's own cull
         nlist = __ldg(lst_g);
         SEG_DCHECK(nlist >= 0 && nlist <= p.T);
 #if SEG_EARLY_TMA
@@ -734,33 +723,12 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         if (STATS) cnt[ST_FIBERS] = inrange ? 1 : 0;
     }
     __syncthreads();
-    __shared__ int s_cull_n;   // fused: the window's list length
-    if (p.fused) {
-        // a2, fused: k_cull's body for this CTA's window, its fibers from the planes just ingested, in the ring's
-        // shared memory (no tile has been copied yet); every thread takes part (the producer warp without fibers).
-        // Its ordered list and seed codes go to global memory like k_cull's and are read back with ld.global.cg.
-        const bool okc = consumer && inrange && !isnan(fm[lane].w);
-        const float4 e4 = consumer ? fe[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 z4 = consumer ? fez[lane] : e4;
-        const float4 m4 = consumer ? fm[lane] : e4;
-        uint32_t *cs = reinterpret_cast<uint32_t *>(smem + L.ring);
-        float4 *cb = reinterpret_cast<float4 *>(smem + L.ring + ((cull_smem_bytes(p.T, p.B) + 15) & ~(size_t)15));
-        cull_window(p, cta, threadIdx.x, NTHREADS, okc, (consumer && inrange) ? fidx : -1, e4,
-                    make_float2(z4.x, z4.y), make_float4(m4.x, m4.y, m4.z, 0.f), cs, cb, s_cull_n);
-        __syncthreads();
-        if (threadIdx.x == FPC) {
-            nlist = s_cull_n;
-            // the ring's bytes were written through the generic proxy; the TMA copies write them through the
-            // async proxy
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-    }
     // the seed (exact mode): k_cull named for each fiber the best-first winner of its nearest tile; the lane
     // evaluates that one candidate in full -- its fiber from shared memory, the centroid's 21 points from
     // the centroid-major copy -- with k_classify's arithmetic, and starts from its key.  It is one of the
     // candidates the tile stream would evaluate, so the result cannot change; a good start prunes the rest.
     if (consumer && p.seed_code && inrange && !isnan(fm[lane].w)) {
-        const int code = p.fused ? __ldcg(p.seed_code + fidx) : __ldg(p.seed_code + fidx);
+        const int code = __ldg(p.seed_code + fidx);
         if (code >= 0) {
             const int tn = code >> 6, c = (code >> 1) & 31;
             int o = code & 1;
@@ -809,7 +777,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) k_classify(ClassifyPara
         if (lane == 0) {
             int k = kpre;
             for (; k < nlist; ++k) {
-                const int t = p.fused ? __ldcg(lst_g + 1 + k) : __ldg(lst_g + 1 + k);
+                const int t = __ldg(lst_g + 1 + k);
                 SEG_DCHECK(t >= 0 && t < p.T);
                 const int s = k % STAGES, u = k / STAGES;
                 if (u > 0) mbar_sleep_wait(empty + s, (u - 1) & 1);
@@ -947,7 +915,7 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
         };
         long long tc0 = 0;
         if (STATS) tc0 = clock64();
-        const int klim = SEG_NLIST ? (p.fused ? s_cull_n : s_nlist) : 0x7fffffff;
+        const int klim = SEG_NLIST ? s_nlist : 0x7fffffff;
         for (int k = 0; k < klim; ++k) {
             const int s = k % STAGES, u = k / STAGES;
             long long tw0 = 0;
@@ -1216,22 +1184,18 @@ r = fmaxf(r, d2(a.x, a.y, fz[mid_slot(i) * PP + fl], make_float4(b.x, b.y, cz[mi
 __host__ __device__ inline size_t cull_smem_bytes(int T, int B) {
     return sizeof(uint32_t) * (size_t)(((T + 31) >> 5) + ((B + 31) >> 5) + T) + sizeof(uint16_t) * (size_t)T;
 }
-// The body of k_cull for one fiber window: run by k_cull's 256 threads (one fiber each) or, fused, by all
-// NTHREADS threads of k_classify's CTA right after its ingest (the producer warp without fibers).  tid / nthr: the
-// thread's index and the thread count; ok / myfidx / E / Ez / F10: the thread's fiber (finite, caller index,
-// points 0 / 10 / 20); sbits: [twords + bwords + T] u32 + [T] u16 of shared memory; sbs: bpad float4 of shared
-// memory; nlist: a shared int.  Writes the window's ordered list to p.tile_bits and the seed codes to p.seed_code.
-__device__ __forceinline__ void cull_window(const ClassifyParams &p, const int win, const int tid, const int nthr,
-                                            bool ok, const int myfidx, float4 E, float2 Ez, float4 F10,
-                                            uint32_t *sbits, float4 *sbs, int &nlist) {
+__global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyParams p) {
     // smem: [twords] tile bits, [bwords] bundle bits, [T] per-tile priority, [T] list (u16)
+    extern __shared__ __align__(16) uint32_t sbits[];
     const int twords = (p.T + 31) >> 5, bwords = (p.B + 31) >> 5;
     uint32_t *tb = sbits, *bb = sbits + twords, *prio = bb + bwords;
     uint16_t *lst = reinterpret_cast<uint16_t *>(prio + p.T);
+    __shared__ int nlist;
     // per bundle the point-10 sphere grown by the bundle threshold: (centre, R^2); an empty bundle (and
     // the padding up to a multiple of 32) gets a centre at 1e30 so that no fiber passes it
-    for (int i = tid; i < twords + bwords + p.T; i += nthr) sbits[i] = 0;
-    if (SEG_CULL_APPEND && tid == 0) nlist = 0;
+    __shared__ float4 sbs[MAX_SMEM_BUNDLES];
+    for (int i = threadIdx.x; i < twords + bwords + p.T; i += FPC) sbits[i] = 0;
+    if (SEG_CULL_APPEND && threadIdx.x == 0) nlist = 0;
     const bool stage_bh = p.B <= MAX_SMEM_BUNDLES;
     auto bsphere = [&](int b) {
         if (b >= p.B) return make_float4(1e30f, 1e30f, 1e30f, 0.f);
@@ -1241,8 +1205,21 @@ __device__ __forceinline__ void cull_window(const ClassifyParams &p, const int w
     };
     const int bpad = (p.B + 31) & ~31;
     if (stage_bh)
-        for (int i = tid; i < bpad; i += nthr) sbs[i] = bsphere(i);
-    const int lane = tid & 31;
+        for (int i = threadIdx.x; i < bpad; i += FPC) sbs[i] = bsphere(i);
+    const int lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * FPC + threadIdx.x;
+    bool ok = gi < p.n;
+    float4 E = make_float4(0.f, 0.f, 0.f, 0.f), F10 = E;
+    float2 Ez = make_float2(0.f, 0.f);
+    if (ok) {
+        const int fidx = p.perm ? __ldg(p.perm + gi) : gi;
+        const float *src = p.fibers + (size_t)fidx * (3 * NPTS);
+        E = make_float4(__ldg(src + 0), __ldg(src + 60), __ldg(src + 1), __ldg(src + 61));
+        Ez = make_float2(__ldg(src + 2), __ldg(src + 62));
+        F10 = make_float4(__ldg(src + 30), __ldg(src + 31), __ldg(src + 32), 0.f);
+        ok = isfinite(E.x) && isfinite(E.y) && isfinite(E.z) && isfinite(E.w) && isfinite(Ez.x) && isfinite(Ez.y) &&
+             isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
+    }
     if (!ok) F10 = make_float4(__int_as_float(0x7fffffff), 0.f, 0.f, 0.f);   // NaN: every bound test fails
     float nd2 = INFINITY;   // each fiber's nearest tile by its sphere centres: the seed's tile
     int ntile = -1;
@@ -1375,6 +1352,7 @@ __device__ __forceinline__ void cull_window(const ClassifyParams &p, const int w
     // from it.  Warp-cooperative: lane = centroid for the 3-point scores (the tile's rows stay in registers
     // while consecutive fibers share the tile); only points 0 / 10 / 20, already in registers, are needed.
     if (p.seed_code) {
+        const int myfidx = gi < p.n ? (p.perm ? __ldg(p.perm + gi) : gi) : -1;
         const bool want = myfidx >= 0 && ntile >= 0;
         if (myfidx >= 0 && !want) p.seed_code[myfidx] = -1;
 #if defined(SEG_EXP) && (SEG_EXP == 4 || SEG_EXP == 5)
@@ -1423,7 +1401,7 @@ seed_done:
     __syncthreads();
 #if !SEG_CULL_APPEND
     // the CTA's tiles from the bit set (warp 0: prefix over the words), in tile order
-    if (tid < 32) {
+    if (threadIdx.x < 32) {
         int base = 0;
         for (int w0 = 0; w0 < twords; w0 += 32) {
             const uint32_t bits = w0 + lane < twords ? tb[w0 + lane] : 0u;
@@ -1453,12 +1431,12 @@ seed_done:
     // gives the same result (the (d^2, bundle) minimum is order-independent); a good order makes
     // the running best tight early, which prunes the later tiles.
     const int n = nlist;
-    uint16_t *out = reinterpret_cast<uint16_t *>(p.tile_bits) + (size_t)win * cull_stride(p.T);
-    if (tid == 0) {
+    uint16_t *out = reinterpret_cast<uint16_t *>(p.tile_bits) + (size_t)blockIdx.x * cull_stride(p.T);
+    if (threadIdx.x == 0) {
         out[0] = (uint16_t)n;
-        if (p.cta_order) p.cta_order[win] = n;   // k_cta_order's input (LPT launch order; not in fused mode)
+        if (p.cta_order) p.cta_order[blockIdx.x] = n;   // k_cta_order's input (LPT launch order)
     }
-    for (int i = tid; i < n; i += nthr) {
+    for (int i = threadIdx.x; i < n; i += FPC) {
         const int ti = lst[i];
         const uint32_t ki = prio[ti];
         int rank = 0;
@@ -1471,27 +1449,6 @@ seed_done:
         SEG_DCHECK(rank < n);
         out[1 + rank] = (uint16_t)ti;
     }
-}
-
-__global__ void __launch_bounds__(FPC, SEG_CULL_MAXREG_CTAS) k_cull(ClassifyParams p) {
-    extern __shared__ __align__(16) uint32_t sbits[];
-    __shared__ int nlist;
-    __shared__ float4 sbs[MAX_SMEM_BUNDLES];
-    const int gi = blockIdx.x * FPC + threadIdx.x;
-    bool ok = gi < p.n;
-    int myfidx = -1;
-    float4 E = make_float4(0.f, 0.f, 0.f, 0.f), F10 = E;
-    float2 Ez = make_float2(0.f, 0.f);
-    if (ok) {
-        myfidx = p.perm ? __ldg(p.perm + gi) : gi;
-        const float *src = p.fibers + (size_t)myfidx * (3 * NPTS);
-        E = make_float4(__ldg(src + 0), __ldg(src + 60), __ldg(src + 1), __ldg(src + 61));
-        Ez = make_float2(__ldg(src + 2), __ldg(src + 62));
-        F10 = make_float4(__ldg(src + 30), __ldg(src + 31), __ldg(src + 32), 0.f);
-        ok = isfinite(E.x) && isfinite(E.y) && isfinite(E.z) && isfinite(E.w) && isfinite(Ez.x) && isfinite(Ez.y) &&
-             isfinite(F10.x) && isfinite(F10.y) && isfinite(F10.z);
-    }
-    cull_window(p, blockIdx.x, threadIdx.x, FPC, ok, myfidx, E, Ez, F10, sbits, sbs, nlist);
 }
 
 // row f4: keys -> (label, dist), the decode of an atlas-sharded run
@@ -1594,27 +1551,10 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
     const size_t smem = classify_smem_bytes(p.B, p.T);
     const int grid = (p.n + FPC - 1) / FPC;
     const size_t cull_smem = cull_smem_bytes(p.T, p.B);
-    // fused (grids of at most one wave, i.e. small inputs): k_classify culls its own window, in the ring's shared
-    // memory, instead of a k_cull launch before it.  For larger grids the separate kernel wins: inside k_classify
-    // the cull runs at k_classify's 18 warps per SM instead of k_cull's 40 (cfg 3: 5.78 vs 5.31 ms per step;
-    // cfg 0: 0.059 vs 0.074 ms)
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        sms = 0;
-    const bool fuse = SEG_FUSE && grid <= sms * CTAS_PER_SM && p.B <= MAX_SMEM_BUNDLES &&
-                      ((cull_smem + 15) & ~(size_t)15) + sizeof(float4) * (size_t)((p.B + 31) & ~31) <=
-                          (size_t)STAGES * TILE_STRIDE_BYTES;
-    ClassifyParams q = p;
-    cudaError_t e = cudaSuccess;
-    if (fuse) {
-        q.fused = 1;
-        q.cta_order = nullptr;
-    } else {
-        e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
-        if (e != cudaSuccess) return e;
-        k_cull<<<grid, FPC, cull_smem, s>>>(p);
-        if (p.cta_order) k_cta_order<<<1, 1024, 0, s>>>(grid, p.T, p.cta_order);
-    }
+    cudaError_t e = cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cull_smem);
+    if (e != cudaSuccess) return e;
+    k_cull<<<grid, FPC, cull_smem, s>>>(p);
+    if (p.cta_order) k_cta_order<<<1, 1024, 0, s>>>(grid, p.T, p.cta_order);
     if (after_cull) {
         e = cudaEventRecord(after_cull, s);
         if (e != cudaSuccess) return e;
@@ -1622,7 +1562,7 @@ cudaError_t launch_classify(const ClassifyParams &p, bool stats, cudaStream_t s,
     auto go = [&](auto kern) {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (r != cudaSuccess) return r;
-        kern<<<grid, NTHREADS, smem, s>>>(q);
+        kern<<<grid, NTHREADS, smem, s>>>(p);
         return cudaSuccess;
     };
     if (p.masks) e = stats ? go(k_classify<true, false, true>) : go(k_classify<false, false, true>);

@@ -136,7 +136,6 @@ struct ClassifyParams {
     int32_t *cta_order = nullptr;  // nullable [grid]: k_classify's CTA i works on fiber window cta_order[i]
     uint32_t *masks = nullptr;     // nullable [n][mwords]: multi-label output (row f4), bit b = bundle b within threshold
     int mwords = 0;
-    int fused = 0;                 // k_classify runs its own window's cull first (k_cull's body, SEG_FUSE)
 };
 
 struct MortonParams {
