@@ -643,10 +643,14 @@ int classify_device(const seg_atlas *a, const float *fib, int n, int32_t *lab, f
         SEG_CUDA(sc.get(&cp.seed_code, sizeof(int32_t) * (size_t)n), "seg_classify: scratch allocation");
     }
 #ifndef SEG_NO_LPT
+#ifndef SEG_LPT_WAVES
+#define SEG_LPT_WAVES 64
+#endif
     {   // longest-list-first launch order (k_cta_order) where the grid's last wave is a visible share:
-        // up to 64 waves of 2 CTAs per SM (cfg 1: -9%, cfg 3: -0.4%; cfg 4's 105 waves: +0.2% without it)
+        // up to 64 waves of 2 CTAs per SM (cfg 1: -9%, cfg 3: -0.4%; cfg 4's 105 waves: +0.2% without it, and
+        // again +0.15% with it at the end of round 2 -- the ordering kernel costs what the order saves)
         const int grid = (int)((n + classify_fibers_per_cta() - 1) / classify_fibers_per_cta());
-        if (grid <= 64 * 2 * a->sms)
+        if (grid <= SEG_LPT_WAVES * 2 * a->sms)
             SEG_CUDA(sc.get(&cp.cta_order, sizeof(int32_t) * (size_t)grid), "seg_classify: scratch allocation");
     }
 #endif
